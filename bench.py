@@ -1,0 +1,318 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 EmptyHeaded hot path (BASELINE.json metric:
+"triangles counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)").
+
+One STEP = one pass of the whole hot path over
+one synthetic input: eh_load_edges (canonicalise, radix sort, dedup, degree
+rank, orient, CSR, set layouts, work lists) + eh_count_triangles + eh_free.
+Workload: C3 = RMAT scale 22, edge factor 16, seed 3 (BASELINE.json
+configs[2], the configuration the ">= 40 % of HBM roofline" target names).
+
+  value  = input edges / device time of one step (inputs resident in HBM)
+  e2e    = the same metric through the C ABI with HOST (pinned) inputs: the
+           H2D copy of the edge list and the 8-byte D2H of the count are inside
+           the timed region
+  roofline (dominant kernel = the triangle count): achieved = B_tri(tau=32)
+           (computed exactly at load: eh_stats.alg_bytes_tri)
+           / device time of eh_count_triangles; peak = MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline = the CPU oracle (oracle/, untuned) on a bounded sample of C3
+
+`--impl reference` times the oracle alone as the reference arm.
+Multi-GPU: the path does not shard (north star "one GPU"):
+`--gpus N` under torchrun runs N independent replicas ("replicas only",
+DESIGN.md); value = edges processed by all ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (input generator; no method arithmetic)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("nccl")
+        return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
+    return None, 0, 1, 0
+
+
+def _max_over_ranks(dist, val: float, device) -> float:
+    if dist is None:
+        return val
+    import torch
+    t = torch.tensor([val], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _flush_l2(buf):
+    buf.add_(1)  # 512 MiB write: > 2x the 126 MB L2
+
+
+# ------------------------------------------------------------------ CPU oracle --
+def _oracle_sample(src, dst, frac_slices: int = 16, slices: int = 1):
+    """Oracle ingest on the full input, then the triangle loop over `slices` of
+    `frac_slices` equal slices of the outer x loop; returns (t_ingest, t_count_est,
+    threads, description)."""
+    import oracle
+    threads = oracle.default_threads()
+    t0 = time.perf_counter()
+    g = oracle.Graph(src, dst)
+    t_ing = time.perf_counter() - t0
+    nv = g.n_vertices
+    t0 = time.perf_counter()
+    for k in range(slices):
+        g.count_triangles_range(nv * k // frac_slices, nv * (k + 1) // frac_slices, threads)
+    t_cnt = (time.perf_counter() - t0) * frac_slices / slices
+    g.close()
+    return g, t_ing, t_cnt, threads
+
+
+def run_reference(args, cfg, src, dst, n_in):
+    """Reference arm: the CPU oracle as it stands on this host's cores."""
+    import oracle
+    dist, rank, ws, _ = _dist()
+    if rank != 0:
+        return
+    threads = oracle.default_threads()
+    t0 = time.perf_counter()
+    g = oracle.Graph(src, dst)
+    t_ing = time.perf_counter() - t0
+    nv = g.n_vertices
+    S = 64  # each step: 1/64 of the outer x loop + 1/64 of the (once-measured) ingest time
+    times = []
+    for i in range(args.warmup + args.steps):
+        k = i % S
+        t0 = time.perf_counter()
+        g.count_triangles_range(nv * k // S, nv * (k + 1) // S, threads)
+        dt = time.perf_counter() - t0 + t_ing / S
+        if i >= args.warmup:
+            times.append(dt)
+    g.close()
+    step_full = statistics.mean(times) * S  # estimated full-workload time
+    value = n_in / step_full
+    sample = (f"oracle ingest of the full {cfg.name} input timed once ({t_ing:.2f} s); each step = one 1/{S} "
+              f"slice of the outer x loop of the triangle nest + 1/{S} of the ingest time; value = n_in / "
+              f"(64 x mean step)")
+    line = {"impl": "reference", "metric": "triangles counted: input edges/sec", "value": value,
+            "unit": "input edges/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, seed {cfg.seed}",
+                       "n_input": n_in},
+            "cpu_baseline": {"value": value, "unit": "input edges/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "input edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm --
+def run_gpu(args, cfg, src, dst, n_in):
+    import torch
+    import paper_1503_02368_b200 as eh
+
+    dist, rank, ws, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    peak, peak_kind = _peaks()
+
+    # inputs resident in HBM before the timed region (value); pinned host copies (e2e)
+    d_src = torch.from_numpy(src.view(np.int32)).to(dev)
+    d_dst = torch.from_numpy(dst.view(np.int32)).to(dev)
+    h_src = torch.from_numpy(src.view(np.int32)).pin_memory()
+    h_dst = torch.from_numpy(dst.view(np.int32)).pin_memory()
+    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB
+    torch.cuda.synchronize()
+
+    def one_step(host: bool):
+        """Returns (t_step_ms, t_count_ms, count, stats)."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            if host:
+                g = eh.Graph(h_src, h_dst, stream=stream)
+            else:
+                g = eh.Graph(d_src, d_dst, stream=stream)
+            ev[1].record(stream)
+            c = g.count_triangles()
+            ev[2].record(stream)
+            st = g.stats()
+            g.close()
+        stream.synchronize()
+        return ev[0].elapsed_time(ev[2]), ev[1].elapsed_time(ev[2]), c, st
+
+    # warm-up
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            _flush_l2(flush)
+        one_step(False)
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = eh.launch_count()
+    step_ms, count_ms, counts = [], [], set()
+    st = None
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            _flush_l2(flush)  # outside the per-step events
+        t, tc, c, st = one_step(False)
+        step_ms.append(t)
+        count_ms.append(tc)
+        counts.add(c)
+    launches = (eh.launch_count() - l0) / max(1, args.steps)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    # e2e through the C ABI with host buffers (H2D inside the timed region)
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        with torch.cuda.stream(stream):
+            _flush_l2(flush)
+        t, _, c, _ = one_step(True)
+        e2e_ms.append(t)
+        counts.add(c)
+    if len(counts) != 1:
+        raise RuntimeError(f"non-deterministic triangle counts: {counts}")
+    T = counts.pop()
+    mean_step = statistics.mean(step_ms)
+    mean_count = statistics.mean(count_ms)
+    mean_e2e = statistics.mean(e2e_ms)
+    mean_step_max = _max_over_ranks(dist, mean_step, dev)
+    mean_e2e_max = _max_over_ranks(dist, mean_e2e, dev)
+    if rank != 0:
+        return
+    value = ws * n_in / (mean_step_max / 1e3)
+    achieved = st.alg_bytes_tri / (mean_count / 1e3) / 1e9
+    line = {
+        "metric": "triangles counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)",
+        "value": value, "unit": "input edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean_step_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, "
+                               f"(a,b,c)=(.57,.19,.19), seed {cfg.seed}; triangle count",
+                   "n_input": n_in, "m_undirected": st.m_undirected, "n_active": st.n_active,
+                   "parallelism": "replicas only" if ws > 1 else "1 GPU",
+                   "l2": "512 MiB flush write between timed steps (outside the per-step events); inputs 537 MB > L2",
+                   "step": "eh_load_edges(device inputs) + eh_count_triangles + eh_free"},
+        "triangles": T,
+        "count_ms": mean_count, "load_ms": mean_step - mean_count,
+        "count_edges_per_s": n_in / (mean_count / 1e3),
+        "triangles_per_s": T / (mean_count / 1e3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind, "kernel": "k_tri_*  (eh_count_triangles)",
+                     "alg_bytes_per_launch": st.alg_bytes_tri},
+        "e2e": {"value": ws * n_in / (mean_e2e_max / 1e3), "unit": "input edges/s",
+                "h2d_bytes_per_step": 8 * n_in, "d2h_bytes_per_step": 8},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        og, t_ing, t_cnt, threads = _oracle_sample(src, dst, frac_slices=16, slices=1)
+        line["cpu_baseline"] = {"value": n_in / (t_ing + t_cnt), "unit": "input edges/s", "cores": threads,
+                                "kind": "oracle",
+                                "sample": f"oracle ingest of the full {cfg.name} input ({t_ing:.1f} s) + the triangle "
+                                          f"loop over 1/16 of the outer x loop, scaled x16 ({t_cnt:.1f} s est.)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="eh", choices=["eh", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "eh":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    cfg = synth.CONFIGS[args.config]
+    src, dst = cfg.generate()
+    n_in = int(src.size)
+    if args.impl == "reference":
+        run_reference(args, cfg, src, dst, n_in)
+    else:
+        run_gpu(args, cfg, src, dst, n_in)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * eh.h -- C ABI of the B200-native EmptyHeaded hot path (arXiv 1503.02368).
+ *
+ * The library (paper_1503_02368_b200/lib/libeh.so, CUDA sm_100a) implements
+ * the worst-case-optimal Generic-Join over a trie of the Edge relation
+ * (Alg. `fig:worst_case`) for two COUNT(*) queries:
+ *
+ *   Triangle(x,y,z) :- R(x,y),S(y,z),T(x,z).
+ *   4Clique(x,y,z,w) :- R(x,y),S(y,z),T(x,z),U(x,w),V(y,w),Q(z,w). PAPER.md:217
+ *
+ * with R = S = ... = the symmetrically pruned Edge relation
+ * and COUNT(*) aggregated as `w:long`.  Everything below this
+ * header runs on one GPU as hand-written CUDA kernels; there is no CPU
+ * fallback: every entry point fails (returns an error) when no CUDA device is
+ * usable.
+ *
+ * Conventions for every function:
+ *  - fixed-width integers only; no C++ types cross the boundary;
+ *  - synchronous with respect to the calling host thread;
+ *  - errors are reported by the return value (NULL, EH_COUNT_ERROR or a
+ *    negative EH_E* code) and detailed by eh_last_status() / eh_last_error(),
+ *    which are thread-local and valid until the next call on that thread;
+ *  - a graph handle is immutable after load and may be counted repeatedly;
+ *    concurrent calls on ONE handle from several threads are not supported.
+ */
+#ifndef EH_H_
+#define EH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct eh_graph eh_graph; /* opaque; owns all device memory of one loaded graph */
+
+enum {
+  EH_OK = 0,
+  EH_EINVAL = -1,     /* bad argument (NULL pointer with n > 0, bad flags, ...) */
+  EH_ENOMEM = -2,     /* device allocation failed (or the allocator hook returned NULL) */
+  EH_ECUDA = -3,      /* a CUDA runtime error (no device, launch failure, ...) */
+  EH_EUNSORTED = -4   /* eh_intersect input not strictly increasing */
+};
+
+/* Unreachable as a count: T <= (sqrt(2)/3) m^1.5 and K4 < C(sqrt(2m)+1, 4) << 2^64. */
+#define EH_COUNT_ERROR UINT64_MAX
+
+#define EH_INPUT_ON_DEVICE 0x1u /* src/dst are device pointers (else host memory, pageable or pinned) */
+#define EH_SET_DEVICE      0x2u /* use cfg->device instead of the current device */
+#define EH_ALL_UINT        0x4u /* relation-level layout, the paper's "-R" ablation: no bitsets */
+
+/* Load-time configuration.  A zero-initialised struct means "defaults". */
+typedef struct {
+  /* Set-level layout optimizer: a set S becomes a bitset iff
+   * span(S) = max - min + 1 < bitset_tau * |S| (strict; u64 arithmetic).
+   * 0 -> 32 (reading c10; the paper's AVX register is tau = 256). */
+  uint32_t bitset_tau;
+  int32_t device; /* CUDA ordinal, honoured only with EH_SET_DEVICE */
+  void* stream;   /* cudaStream_t used for all work; NULL -> a library-owned stream */
+  /* Optional device allocator (e.g. the PyTorch caching allocator).  Both or
+   * neither must be set.  dev_alloc returning NULL makes the call fail with EH_ENOMEM. */
+  void* (*dev_alloc)(size_t bytes, void* stream, void* ctx);
+  void (*dev_free)(void* ptr, void* stream, void* ctx);
+  void* alloc_ctx;
+  uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT */
+  uint32_t bin_small_max;  /* count-kernel work classes; 0 -> tuned defaults. */
+  uint32_t bin_large_min;  /* bin_small_max = UINT32_MAX forces every vertex into the smallest class,
+                              bin_large_min = 1 forces every vertex into the largest class. */
+  uint32_t min_bitset_card;/* bitset only if |S| >= this (reading c15); 0 -> 2 */
+} eh_config;
+
+/* eh_stats: filled by eh_graph_stats (bench / tests). */
+typedef struct {
+  uint64_t n_input;        /* input tuples */
+  uint64_t m_undirected;   /* distinct undirected edges without self-loops = |E+| */
+  uint64_t n_active;       /* non-isolated vertices (the rank space is [0, n_active)) */
+  uint64_t max_out_degree; /* max |N+(x)| */
+  uint64_t n_bitset_sets;  /* sets stored with the bitset layout */
+  uint64_t bitset_words;   /* 32-bit words in the bitset pool */
+  uint64_t device_bytes;   /* device memory owned by the handle */
+  uint64_t alg_bytes_tri;  /* B_tri(tau) of SURVEY.md §8(d): 8(n+1) + sum_x bytes(N+(x)) + sum_(x,y) bytes(N+(y)) */
+  uint64_t wedge_work;     /* sum over (x,y) in E+ of |N+(x) after y| (min-property side) */
+} eh_stats;
+
+/*
+ * eh_load_edges / eh_load_edges_ex -- build the trie of the Edge relation.
+ *
+ * PAPER.md:281-285 (dictionary encoding to 32-bit ids; sets of distinct values
+ * grouped by parent), PAPER.md:799-800 (symmetric pruning, ids by degree),
+ * PAPER.md:730 (set-level uint/bitset layout).
+ *
+ *  src, dst : n undirected pairs (src[i], dst[i]); any uint32 value is a valid id,
+ *             0xFFFFFFFF included.  Self-loops are dropped; duplicates and
+ *             reversed pairs collapse.  Host pointers unless cfg->flags has
+ *             EH_INPUT_ON_DEVICE.  Borrowed for the call only (copied).
+ *  n        : number of pairs; n = 0 gives a valid empty graph (counts 0).
+ *  cfg      : may be NULL (defaults).
+ * Returns a handle owning all device memory until eh_free, or NULL on error
+ * (EH_EINVAL: NULL src/dst with n > 0, one allocator hook without the other;
+ *  EH_ENOMEM; EH_ECUDA).
+ */
+eh_graph* eh_load_edges(const uint32_t* src, const uint32_t* dst, uint64_t n);
+eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg);
+
+/*
+ * eh_count_triangles -- COUNT(*) of Triangle(x,y,z) on the pruned relation:
+ * the number of 3-vertex sets whose three pairs are edges (each counted once).
+ * Generic-Join loop nest PAPER.md:538-542.  Returns EH_COUNT_ERROR on error
+ * (EH_EINVAL for g == NULL, EH_ECUDA).
+ */
+uint64_t eh_count_triangles(eh_graph* g);
+
+/*
+ * eh_count_4cliques -- COUNT(*) of 4Clique(x,y,z,w):
+ * the number of 4-vertex sets whose six pairs are edges, each counted once.
+ * Returns EH_COUNT_ERROR on error.
+ */
+uint64_t eh_count_4cliques(eh_graph* g);
+
+/*
+ * eh_intersect -- the set operation "xs cap ys" of Table `lst:eh_operators`
+ * (PAPER.md:515-516), with the paper's layout-dependent algorithms
+ * (PAPER.md:628-642): each input gets the set-level layout (uint or bitset,
+ * tau = 32); uint cap uint uses a merge when the cardinality ratio is <= 32
+ * and binary search (galloping) otherwise; uint cap bitset probes the bitset;
+ * bitset cap bitset ANDs the overlapping words.
+ *
+ *  a[0..na), b[0..nb) : strictly increasing uint32 (host or device memory,
+ *                       detected per pointer).  Validated in O(na + nb).
+ *  out                : NULL (count only) or caller-owned room for
+ *                       min(na, nb) uint32 (host or device memory); receives
+ *                       the intersection in increasing order.
+ * Returns |a cap b| >= 0, or EH_EINVAL (NULL with n > 0), EH_EUNSORTED,
+ * EH_ENOMEM, EH_ECUDA.
+ */
+int64_t eh_intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);
+
+/* Statistics of a loaded graph.  Returns EH_OK or EH_EINVAL. */
+int eh_graph_stats(const eh_graph* g, eh_stats* out);
+
+/*
+ * eh_graph_export -- copy the oriented trie to HOST memory (tests, debugging).
+ *  row_ptr [n_active+1] : out-list offsets (unpadded, in elements)
+ *  col     [m]          : out-neighbours in rank space, each list strictly increasing
+ *  orig_id [n_active]   : original uint32 id of each rank
+ *  is_bitset[n_active]  : 1 if the set N+(rank) uses the bitset layout
+ * Any pointer may be NULL.  Returns EH_OK, EH_EINVAL or EH_ECUDA.
+ */
+int eh_graph_export(const eh_graph* g, uint64_t* row_ptr, uint32_t* col, uint32_t* orig_id, uint8_t* is_bitset);
+
+/* Release a handle and all its device memory.  NULL-safe. */
+void eh_free(eh_graph* g);
+
+/* Number of CUDA kernels this library has launched in this process (diagnostics; bench.py). */
+uint64_t eh_launch_count(void);
+
+int eh_last_status(void);        /* thread-local status of the last call (EH_OK or EH_E*) */
+const char* eh_last_error(void); /* thread-local message, "" if none */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EH_H_ */

@@ -1,0 +1,206 @@
+// eh_api.cu -- the extern "C" boundary declared in include/eh.h.
+//
+// Every entry point: validate arguments, select the device, run the CUDA path,
+// translate internal exceptions into the documented return codes and the
+// thread-local status / message.  There is no CPU fallback anywhere.
+#include "eh_internal.cuh"
+
+#include <cstring>
+
+namespace eh {
+std::atomic<unsigned long long> g_launches{0};
+}
+
+namespace {
+
+thread_local int t_status = EH_OK;
+thread_local char t_msg[512] = "";
+
+void set_status(int code, const char* msg) {
+  t_status = code;
+  std::snprintf(t_msg, sizeof t_msg, "%s", msg ? msg : "");
+}
+void ok() { set_status(EH_OK, ""); }
+
+template <class R, class F>
+R guarded(R on_error, F&& f) {
+  try {
+    R r = f();
+    ok();
+    return r;
+  } catch (const eh::Error& e) {
+    set_status(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    set_status(EH_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    set_status(EH_ECUDA, e.what());
+  }
+  return on_error;
+}
+
+void destroy(eh_graph* g) {
+  if (!g) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  for (void* p : g->owned) g->alloc.release(p);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->h_counter) cudaFreeHost(g->h_counter);
+  if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete g;
+}
+
+struct DeviceGuard {  // restores the caller's current device
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    EH_CUDA(cudaGetDevice(&prev));
+    if (dev != prev) EH_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+extern "C" {
+
+eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg) {
+  return guarded<eh_graph*>(nullptr, [&]() -> eh_graph* {
+    eh_config c;
+    std::memset(&c, 0, sizeof c);
+    if (cfg) c = *cfg;
+    if (n && (!src || !dst)) eh::fail(EH_EINVAL, "eh_load_edges: NULL src/dst with n = %llu", (unsigned long long)n);
+    if ((c.dev_alloc == nullptr) != (c.dev_free == nullptr))
+      eh::fail(EH_EINVAL, "eh_load_edges: dev_alloc and dev_free must be set together");
+    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT))
+      eh::fail(EH_EINVAL, "eh_load_edges: unknown flags 0x%x", c.flags);
+    int ndev = 0;
+    EH_CUDA(cudaGetDeviceCount(&ndev));
+    if (ndev <= 0) eh::fail(EH_ECUDA, "no CUDA device");
+    int dev = 0;
+    EH_CUDA(cudaGetDevice(&dev));
+    if (c.flags & EH_SET_DEVICE) {
+      if (c.device < 0 || c.device >= ndev) eh::fail(EH_EINVAL, "eh_load_edges: bad device %d", c.device);
+      dev = c.device;
+    }
+    DeviceGuard guard(dev);
+    eh_graph* g = new eh_graph();
+    try {
+      g->device = dev;
+      g->flags = c.flags;
+      g->tau = c.bitset_tau ? c.bitset_tau : 32;
+      g->min_bitset_card = c.min_bitset_card ? c.min_bitset_card : 2;
+      g->bin_small_max = c.bin_small_max;
+      g->bin_large_min = c.bin_large_min;
+      if (c.stream) {
+        g->stream = (cudaStream_t)c.stream;
+      } else {
+        EH_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        g->own_stream = true;
+      }
+      g->alloc.hook_alloc = c.dev_alloc;
+      g->alloc.hook_free = c.dev_free;
+      g->alloc.ctx = c.alloc_ctx;
+      g->alloc.stream = g->stream;
+      EH_CUDA(cudaMallocHost(&g->h_counter, 2 * sizeof(unsigned long long)));
+      g->d_counter = (unsigned long long*)g->own(2 * sizeof(unsigned long long));
+      // a1: upload (borrowed inputs are copied)
+      eh::DBuf<uint32_t> in;
+      const uint32_t* d_src = src;
+      const uint32_t* d_dst = dst;
+      if (n && !(c.flags & EH_INPUT_ON_DEVICE)) {
+        in = eh::DBuf<uint32_t>(g->alloc, 2 * n);
+        EH_CUDA(cudaMemcpyAsync(in.p, src, n * 4, cudaMemcpyHostToDevice, g->stream));
+        EH_CUDA(cudaMemcpyAsync(in.p + n, dst, n * 4, cudaMemcpyHostToDevice, g->stream));
+        d_src = in.p;
+        d_dst = in.p + n;
+      }
+      eh::build_trie(g, d_src, d_dst, n);
+      in.reset();
+      eh::build_layouts(g);
+      eh::build_worklists(g);
+      EH_CUDA(cudaStreamSynchronize(g->stream));
+    } catch (...) {
+      destroy(g);
+      throw;
+    }
+    return g;
+  });
+}
+
+eh_graph* eh_load_edges(const uint32_t* src, const uint32_t* dst, uint64_t n) {
+  return eh_load_edges_ex(src, dst, n, nullptr);
+}
+
+uint64_t eh_count_triangles(eh_graph* g) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_triangles: NULL graph");
+    DeviceGuard guard(g->device);
+    return eh::count_triangles(g);
+  });
+}
+
+uint64_t eh_count_4cliques(eh_graph* g) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_4cliques: NULL graph");
+    DeviceGuard guard(g->device);
+    return eh::count_4cliques(g);
+  });
+}
+
+int64_t eh_intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out) {
+  int64_t r = guarded<int64_t>(INT64_MIN, [&]() -> int64_t { return eh::intersect(a, na, b, nb, out); });
+  return r == INT64_MIN ? (int64_t)t_status : r;
+}
+
+int eh_graph_stats(const eh_graph* g, eh_stats* out) {
+  if (!g || !out) {
+    set_status(EH_EINVAL, "eh_graph_stats: NULL argument");
+    return EH_EINVAL;
+  }
+  out->n_input = g->n_input;
+  out->m_undirected = g->m;
+  out->n_active = g->n_act;
+  out->max_out_degree = g->max_dplus;
+  out->n_bitset_sets = g->n_bitsets;
+  out->bitset_words = g->bs_words;
+  out->device_bytes = g->device_bytes;
+  out->alg_bytes_tri = g->alg_bytes_tri;
+  out->wedge_work = g->wedge_work;
+  ok();
+  return EH_OK;
+}
+
+int eh_graph_export(const eh_graph* g, uint64_t* row_ptr, uint32_t* col, uint32_t* orig_id, uint8_t* is_bitset) {
+  return guarded<int>(EH_ECUDA, [&]() -> int {
+    if (!g) eh::fail(EH_EINVAL, "eh_graph_export: NULL graph");
+    DeviceGuard guard(g->device);
+    const uint64_t n = g->n_act;
+    std::vector<uint4> desc(n + 1);
+    EH_CUDA(cudaMemcpyAsync(desc.data(), g->desc, (n + 1) * sizeof(uint4), cudaMemcpyDeviceToHost, g->stream));
+    std::vector<uint32_t> padded(g->col_elems);
+    if (g->col_elems)
+      EH_CUDA(cudaMemcpyAsync(padded.data(), g->col, g->col_elems * 4, cudaMemcpyDeviceToHost, g->stream));
+    if (orig_id && n) EH_CUDA(cudaMemcpyAsync(orig_id, g->orig_id, n * 4, cudaMemcpyDeviceToHost, g->stream));
+    EH_CUDA(cudaStreamSynchronize(g->stream));
+    uint64_t pos = 0;
+    for (uint64_t v = 0; v < n; ++v) {
+      if (row_ptr) row_ptr[v] = pos;
+      if (col) std::memcpy(col + pos, padded.data() + (uint64_t)desc[v].x * 4, (size_t)desc[v].y * 4);
+      if (is_bitset) is_bitset[v] = desc[v + 1].z != desc[v].z;
+      pos += desc[v].y;
+    }
+    if (row_ptr) row_ptr[n] = pos;
+    return EH_OK;
+  });
+}
+
+void eh_free(eh_graph* g) { destroy(g); }
+
+uint64_t eh_launch_count(void) { return eh::g_launches.load(); }
+
+int eh_last_status(void) { return t_status; }
+const char* eh_last_error(void) { return t_msg; }
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// eh_internal.cuh -- internal types, error plumbing and allocation for libeh.
+// Product code (sm_100a).  Shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "eh.h"
+
+namespace eh {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;  // pad value of `col` (masked by length, never by value)
+constexpr int kSMs = 148;
+
+// Internal failures are C++ exceptions caught at the ABI boundary (eh_api.cu).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Error(code, buf);
+}
+
+inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? EH_ENOMEM : EH_ECUDA;
+    cudaGetLastError();  // clear sticky-free errors
+    fail(code, "%s: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  }
+}
+#define EH_CUDA(call) ::eh::check_cuda((call), #call, __FILE__, __LINE__)
+// Every kernel launch is followed by exactly one EH_LAUNCH, which also counts it
+// (eh_launch_count(), used by bench.py's "gpu_launches").
+extern std::atomic<unsigned long long> g_launches;
+#define EH_LAUNCH(what) \
+  (::eh::g_launches.fetch_add(1, std::memory_order_relaxed), \
+   ::eh::check_cuda(cudaGetLastError(), what, __FILE__, __LINE__))
+
+// Device allocator: the caller's hooks (e.g. torch's caching allocator) or cudaMallocAsync.
+struct Allocator {
+  void* (*hook_alloc)(size_t, void*, void*) = nullptr;
+  void (*hook_free)(void*, void*, void*) = nullptr;
+  void* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+
+  void* alloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    void* p = nullptr;
+    if (hook_alloc) {
+      p = hook_alloc(bytes, (void*)stream, ctx);
+      if (!p) fail(EH_ENOMEM, "allocator hook returned NULL for %zu bytes", bytes);
+    } else {
+      cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? EH_ENOMEM : EH_ECUDA, "cudaMallocAsync(%zu): %s", bytes,
+             cudaGetErrorString(e));
+      }
+    }
+    return p;
+  }
+  void release(void* p) {
+    if (!p) return;
+    if (hook_free) hook_free(p, (void*)stream, ctx);
+    else cudaFreeAsync(p, stream);
+  }
+};
+
+// RAII device buffer bound to an Allocator.
+template <typename T>
+struct DBuf {
+  Allocator* a = nullptr;
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(Allocator& al, size_t count) : a(&al), p((T*)al.alloc(count * sizeof(T))), n(count) {}
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : a(o.a), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { reset(); a = o.a; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void reset() { if (p && a) a->release(p); p = nullptr; n = 0; }
+  T* release_ptr() { T* q = p; p = nullptr; n = 0; return q; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+inline uint32_t bitlen(uint64_t v) {  // number of bits needed to represent v (0 -> 0)
+  uint32_t b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = kSMs * 16) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// ---------------------------------------------------------------- primitives
+// (primitives.cu)  device-wide exclusive scan of u32 or u64 counts into u64
+// offsets; the total is written to *d_total (device) when non-null.
+void scan_exclusive_u32(const uint32_t* in, uint64_t* out, uint64_t n, uint64_t* d_total, Allocator& al,
+                        cudaStream_t s);
+void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* d_total, Allocator& al,
+                        cudaStream_t s);
+
+// LSD radix sort of u64 keys over bits [0, key_bits), 8-bit digits, stable.
+// Returns the buffer holding the result (keys or alt).
+uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
+                         cudaStream_t s);
+// Same for u32 keys.
+uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
+                         cudaStream_t s);
+
+template <typename T>
+inline T read_scalar(const T* d, cudaStream_t s) {
+  T h;
+  EH_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace eh
+
+// ------------------------------------------------------------- the handle --
+struct eh_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  eh::Allocator alloc;
+  uint32_t flags = 0, tau = 32, min_bitset_card = 2;
+  uint32_t bin_small_max = 0, bin_large_min = 0;
+
+  uint64_t n_input = 0, m = 0, n_act = 0, max_dplus = 0;
+  uint64_t n_bitsets = 0, bs_words = 0, col_elems = 0;
+  uint64_t alg_bytes_tri = 0, wedge_work = 0;
+
+  // Device trie (rank space).  desc[v] = {col offset in 16-B units, |N+(v)|,
+  // bitset pool offset in 16-B chunks (prefix; n_chunks = desc[v+1].z - desc[v].z),
+  // first 128-bit chunk index of the bitset span}; desc has n_act+1 entries.
+  uint4* desc = nullptr;
+  uint32_t* col = nullptr;      // padded per list to 4 elements with kNone
+  uint32_t* bs = nullptr;       // bitset pool (128-bit aligned chunks at absolute id/128)
+  uint32_t* orig_id = nullptr;  // original id of each rank
+  // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
+  uint32_t* work = nullptr;
+  uint64_t n_work[3] = {0, 0, 0};
+  unsigned long long* d_counter = nullptr;  // 2 x u64 accumulators
+  unsigned long long* h_counter = nullptr;  // pinned host mirror
+
+  std::vector<void*> owned;  // every device allocation above
+  uint64_t device_bytes = 0;
+
+  void* own(size_t bytes) {
+    void* p = alloc.alloc(bytes);
+    owned.push_back(p);
+    device_bytes += (bytes + 255) & ~size_t(255);
+    return p;
+  }
+};
+
+namespace eh {
+// ingest.cu: canonicalise, sort, dedup, degree rank, orient, CSR; fills g->desc/col/orig_id.
+void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n);
+// trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
+void build_layouts(eh_graph* g);
+void build_worklists(eh_graph* g);
+// count_tri.cu / count_k4.cu
+uint64_t count_triangles(eh_graph* g);
+uint64_t count_4cliques(eh_graph* g);
+// intersect.cu
+int64_t intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);
+}  // namespace eh

@@ -1,0 +1,277 @@
+// ingest.cu -- SURVEY.md §8(a) rows a1-a5: upload, canonicalise, radix sort,
+// dedup (= symmetrisation to a simple undirected graph), degree + (degree, id)
+// rank (dictionary encoding), orientation (symmetric pruning) and CSR.
+//
+//  PAPER.md:281-282  dictionary encoding of values to 32-bit ids; "the order of
+//                    dictionary ID assignment affects the density of the sets"
+//  PAPER.md:284      values "grouped into sets of distinct values based on their
+//                    parent attribute"
+//  PAPER.md:799-800  pruning: "each undirected edge is pruned such that
+//                    src_id > dst_id and id's are assigned based upon the degree"
+//  Readings: c2 ascending (deg, id) rank, orient low -> high (a mirror
+//  of the paper's convention; any strict order gives the same counts), c3 ties by
+//  original id, c4 degree = distinct neighbours, c5 self-loops dropped, c6 dedup,
+//  c7 (u,v) == (v,u), c16 any uint32 is a valid id.
+#include "eh_internal.cuh"
+#include "primitives.cuh"
+
+#include <algorithm>
+
+namespace eh {
+
+namespace {
+
+__global__ void k_max_id(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                         uint32_t* __restrict__ out) {
+  uint32_t mx = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    mx = max(mx, max(src[i], dst[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+// Dictionary path: map each id to its index in the sorted distinct id list.
+__global__ void k_dict_map(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n,
+                           const uint32_t* __restrict__ dict, uint64_t nd) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = in[i];
+    uint64_t lo = 0, hi = nd;  // lower_bound
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (dict[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    out[i] = (uint32_t)lo;
+  }
+}
+
+// a1: canonical undirected key (min << b) | max; self-loops -> all-ones sentinel.
+__global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                        uint32_t b, uint64_t* __restrict__ keys) {
+  const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = src[i], v = dst[i];
+    keys[i] = (u == v) ? sentinel : (((uint64_t)min(u, v) << b) | (uint64_t)max(u, v));
+  }
+}
+
+struct UniqueKeyPred {  // a3: first of a run of equal keys, sentinel excluded
+  const uint64_t* k;
+  uint64_t sentinel;
+  __device__ bool operator()(uint64_t i) const { return k[i] != sentinel && (i == 0 || k[i] != k[i - 1]); }
+};
+struct CopyKeyEmit {
+  const uint64_t* k;
+  uint64_t* out;
+  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = k[i]; }
+};
+struct UniqueU32Pred {
+  const uint32_t* k;
+  __device__ bool operator()(uint64_t i) const { return i == 0 || k[i] != k[i - 1]; }
+};
+struct CopyU32Emit {
+  const uint32_t* k;
+  uint32_t* out;
+  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = k[i]; }
+};
+
+// a4: degree = number of distinct neighbours.
+__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint32_t* __restrict__ deg) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    atomicAdd(&deg[k >> b], 1u);
+    atomicAdd(&deg[k & mask], 1u);
+  }
+}
+
+struct ActivePred {
+  const uint32_t* deg;
+  __device__ bool operator()(uint64_t i) const { return deg[i] != 0; }
+};
+struct RankKeyEmit {  // (deg << b) | id, sorted ascending = the (degree, id) order
+  const uint32_t* deg;
+  uint32_t b;
+  uint64_t* out;
+  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = ((uint64_t)deg[i] << b) | i; }
+};
+
+__global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint32_t b, uint32_t* __restrict__ rank,
+                       uint32_t* __restrict__ orig, const uint32_t* __restrict__ dict) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_act; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = (uint32_t)(sorted[r] & mask);
+    rank[id] = (uint32_t)r;
+    orig[r] = dict ? dict[id] : id;
+  }
+}
+
+// a5: orient low rank -> high rank; key (lo << rb) | hi; out-degree histogram.
+__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint32_t* __restrict__ rank,
+                         uint32_t rb, uint64_t* __restrict__ okeys, uint32_t* __restrict__ dplus) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint32_t ru = rank[k >> b], rv = rank[k & mask];
+    const uint32_t lo = min(ru, rv), hi = max(ru, rv);
+    okeys[i] = ((uint64_t)lo << rb) | hi;
+    atomicAdd(&dplus[lo], 1u);
+  }
+}
+
+__global__ void k_pad4(const uint32_t* __restrict__ d, uint64_t n, uint32_t* __restrict__ p4) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    p4[i] = (d[i] + 3u) >> 2;
+}
+
+__global__ void k_fill_col(const uint64_t* __restrict__ okeys, uint64_t m, uint32_t rb,
+                           const uint64_t* __restrict__ row_start, const uint64_t* __restrict__ off16,
+                           uint32_t* __restrict__ col) {
+  const uint64_t mask = (1ull << rb) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = okeys[i];
+    const uint64_t lo = k >> rb;
+    col[off16[lo] * 4 + (i - row_start[lo])] = (uint32_t)(k & mask);
+  }
+}
+
+__global__ void k_desc_base(const uint64_t* __restrict__ off16, const uint32_t* __restrict__ dplus, uint64_t n_act,
+                            uint64_t total16, uint4* __restrict__ desc) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n_act; v += (uint64_t)gridDim.x * blockDim.x) {
+    if (v < n_act) desc[v] = make_uint4((uint32_t)off16[v], dplus[v], 0u, 0u);
+    else desc[v] = make_uint4((uint32_t)total16, 0u, 0u, 0u);
+  }
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ out) {
+  uint32_t mx = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    mx = max(mx, a[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+}  // namespace
+
+void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n) {
+  Allocator& al = g->alloc;
+  cudaStream_t s = g->stream;
+  const unsigned TB = 256;
+  g->n_input = n;
+  if (n == 0) {
+    g->desc = (uint4*)g->own(sizeof(uint4));
+    EH_CUDA(cudaMemsetAsync(g->desc, 0, sizeof(uint4), s));
+    g->col = (uint32_t*)g->own(16);
+    g->orig_id = (uint32_t*)g->own(16);
+    return;
+  }
+  // ---- a1: id space; dictionary-encode if ids are spread out
+  DBuf<uint32_t> dmax(al, 1);
+  EH_CUDA(cudaMemsetAsync(dmax.p, 0, 4, s));
+  k_max_id<<<grid_for(n, TB * 8), TB, 0, s>>>(d_src, d_dst, n, dmax.p);
+  EH_LAUNCH("k_max_id");
+  const uint32_t max_id = read_scalar(dmax.p, s);
+  uint64_t n_ids = (uint64_t)max_id + 1;
+  DBuf<uint32_t> dict, msrc, mdst;
+  const uint32_t* usrc = d_src;
+  const uint32_t* udst = d_dst;
+  if (n_ids > 8 * n + (1ull << 20)) {
+    DBuf<uint32_t> ends(al, 2 * n), alt(al, 2 * n);
+    EH_CUDA(cudaMemcpyAsync(ends.p, d_src, n * 4, cudaMemcpyDeviceToDevice, s));
+    EH_CUDA(cudaMemcpyAsync(ends.p + n, d_dst, n * 4, cudaMemcpyDeviceToDevice, s));
+    uint32_t* sorted = radix_sort_u32(ends.p, alt.p, 2 * n, bitlen(max_id), al, s);
+    DBuf<uint32_t> d(al, 2 * n);
+    n_ids = select_if(2 * n, UniqueU32Pred{sorted}, CopyU32Emit{sorted, d.p}, al, s);
+    dict = std::move(d);
+    msrc = DBuf<uint32_t>(al, n);
+    mdst = DBuf<uint32_t>(al, n);
+    k_dict_map<<<grid_for(n, TB * 4), TB, 0, s>>>(d_src, msrc.p, n, dict.p, n_ids);
+    EH_LAUNCH("k_dict_map");
+    k_dict_map<<<grid_for(n, TB * 4), TB, 0, s>>>(d_dst, mdst.p, n, dict.p, n_ids);
+    EH_LAUNCH("k_dict_map");
+    usrc = msrc.p;
+    udst = mdst.p;
+  }
+  const uint32_t b = std::max<uint32_t>(1, bitlen(n_ids - 1));
+  const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
+
+  // ---- a1/a2: canonical keys + radix sort over the 2b significant bits
+  DBuf<uint64_t> keys(al, n), alt(al, n);
+  k_canon<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, keys.p);
+  EH_LAUNCH("k_canon");
+  msrc.reset();
+  mdst.reset();
+  uint64_t* sk = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);
+  uint64_t* other = (sk == keys.p) ? alt.p : keys.p;
+
+  // ---- a3: dedup (unique adjacent keys, sentinel dropped) -> m distinct undirected edges
+  const uint64_t m = select_if(n, UniqueKeyPred{sk, sentinel}, CopyKeyEmit{sk, other}, al, s);
+  uint64_t* ukeys = other;
+  g->m = m;
+
+  // ---- a4: degree + (degree, id) rank
+  DBuf<uint32_t> deg(al, n_ids);
+  EH_CUDA(cudaMemsetAsync(deg.p, 0, n_ids * 4, s));
+  if (m) {
+    k_degree<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, deg.p);
+    EH_LAUNCH("k_degree");
+  }
+  DBuf<uint32_t> dmaxdeg(al, 1);
+  EH_CUDA(cudaMemsetAsync(dmaxdeg.p, 0, 4, s));
+  k_max_u32<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, dmaxdeg.p);
+  EH_LAUNCH("k_max_u32");
+  const uint32_t max_deg = read_scalar(dmaxdeg.p, s);
+  // rank keys go into the (free) sorted-key buffer `sk`; need n_act <= n (true: n_act <= 2m <= 2n... use own buffer)
+  DBuf<uint64_t> rkeys(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m))),
+      ralt(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m)));
+  const uint64_t n_act = select_if(n_ids, ActivePred{deg.p}, RankKeyEmit{deg.p, b, rkeys.p}, al, s);
+  g->n_act = n_act;
+  uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + bitlen(max_deg), al, s);
+  DBuf<uint32_t>& rank = deg;  // reuse: the degree of every active id is already encoded in rkeys
+  g->orig_id = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);
+  if (n_act) {
+    k_rank<<<grid_for(n_act, TB * 4), TB, 0, s>>>(rsorted, n_act, b, rank.p, g->orig_id, dict.p);
+    EH_LAUNCH("k_rank");
+  }
+  rkeys.reset();
+  ralt.reset();
+
+  // ---- a5: orient + CSR (padded to 16 B per list)
+  const uint32_t rb = std::max<uint32_t>(1, bitlen(n_act ? n_act - 1 : 0));
+  DBuf<uint32_t> dplus(al, std::max<uint64_t>(1, n_act));
+  EH_CUDA(cudaMemsetAsync(dplus.p, 0, std::max<uint64_t>(1, n_act) * 4, s));
+  uint64_t* okeys = sk;  // sk is free once dedup copied the unique keys into `other`
+  DBuf<uint64_t> oalt_buf(al, std::max<uint64_t>(1, m));
+  if (m) {
+    k_orient<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, rb, okeys, dplus.p);
+    EH_LAUNCH("k_orient");
+  }
+  deg.reset();
+  uint64_t* osorted = radix_sort_u64(okeys, oalt_buf.p, m, 2 * rb, al, s);
+  // offsets: unpadded row starts and padded 16-B offsets
+  DBuf<uint64_t> row_start(al, n_act + 1), off16(al, n_act + 1), tot(al, 2);
+  DBuf<uint32_t> p4(al, std::max<uint64_t>(1, n_act));
+  scan_exclusive_u32(dplus.p, row_start.p, n_act, tot.p, al, s);
+  k_pad4<<<grid_for(n_act, TB * 4), TB, 0, s>>>(dplus.p, n_act, p4.p);
+  EH_LAUNCH("k_pad4");
+  scan_exclusive_u32(p4.p, off16.p, n_act, tot.p + 1, al, s);
+  const uint64_t total16 = read_scalar(tot.p + 1, s);
+  if (total16 >= (1ull << 32)) fail(EH_EINVAL, "graph too large: %llu padded 16-B list blocks", (unsigned long long)total16);
+  g->col_elems = total16 * 4;
+  g->col = (uint32_t*)g->own(std::max<uint64_t>(16, total16 * 16));
+  EH_CUDA(cudaMemsetAsync(g->col, 0xFF, std::max<uint64_t>(16, total16 * 16), s));
+  if (m) {
+    k_fill_col<<<grid_for(m, TB * 4), TB, 0, s>>>(osorted, m, rb, row_start.p, off16.p, g->col);
+    EH_LAUNCH("k_fill_col");
+  }
+  g->desc = (uint4*)g->own((n_act + 1) * sizeof(uint4));
+  k_desc_base<<<grid_for(n_act + 1, TB * 4), TB, 0, s>>>(off16.p, dplus.p, n_act, total16, g->desc);
+  EH_LAUNCH("k_desc_base");
+  EH_CUDA(cudaMemsetAsync(dmax.p, 0, 4, s));
+  k_max_u32<<<grid_for(n_act, TB * 8), TB, 0, s>>>(dplus.p, n_act, dmax.p);
+  EH_LAUNCH("k_max_u32");
+  g->max_dplus = read_scalar(dmax.p, s);
+}
+
+}  // namespace eh

@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+All counts are integers, so every comparison is exact equality (BASELINE.json
+north_star: "GPU counts must match the oracle bit-exact").  Inputs are seeded
+and synthetic (synth/), shaped like the paper's workloads.
+"""
+from __future__ import annotations
+
+import json
+import os
+from math import comb
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1503_02368_b200 as eh
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_counts(src, dst, k4=True, **kw):
+    with eh.Graph(src, dst, **kw) as g:
+        t = g.count_triangles()
+        k = g.count_4cliques() if k4 else None
+        return t, k, g.stats()
+
+
+def _oracle(src, dst, k4=True):
+    g = oracle.Graph(src, dst)
+    try:
+        return g.count_triangles(), (g.count_4cliques() if k4 else None), g
+    finally:
+        pass
+
+
+def _check(src, dst, k4=True, **kw):
+    t, k, st = _gpu_counts(src, dst, k4=k4, **kw)
+    ot, ok, og = _oracle(src, dst, k4=k4)
+    assert t == ot, (t, ot)
+    if k4:
+        assert k == ok, (k, ok)
+    assert st.m_undirected == og.m and st.n_active == og.n_vertices and st.max_out_degree == og.max_out_degree
+    og.close()
+    return t, k
+
+
+# ------------------------------------------------------------ golden / closed forms --
+def test_golden_w1_w2(golden_dir):
+    for name in ("w1_worked_example.json", "w2_k5.json"):
+        w = json.load(open(os.path.join(golden_dir, name)))
+        t, k, _ = _gpu_counts(w["src"], w["dst"])
+        assert (t, k) == (w["triangles"], w["four_cliques"])
+
+
+@pytest.mark.parametrize("n", list(range(0, 24)) + [64, 100, 257])
+def test_kn(n):
+    t, k, _ = _gpu_counts(*synth.complete(n))
+    assert t == comb(n, 3) and k == comb(n, 4)
+
+
+def test_k3000_triangles_and_k600_4cliques_above_2_32():
+    t, _, _ = _gpu_counts(*synth.complete(3000), k4=False)
+    assert t == comb(3000, 3) == 4_495_501_000
+    with eh.Graph(*synth.complete(600)) as g:
+        assert g.count_4cliques() == comb(600, 4) == 5_346_164_850
+
+
+@pytest.mark.parametrize("sizes", [(3, 4), (5, 5, 5), (2, 3, 4, 5), (30, 40, 50), (7, 1, 3, 2, 6, 9)])
+def test_multipartite(sizes):
+    t, k, _ = _gpu_counts(*synth.complete_multipartite(sizes))
+    assert t == sum(a * b * c for i, a in enumerate(sizes) for j, b in enumerate(sizes[i + 1:], i + 1)
+                    for c in sizes[j + 1:])
+    assert k == oracle.count_4cliques(*synth.complete_multipartite(sizes))
+
+
+def test_bipartite_and_wheel():
+    for seed in range(3):
+        t, k, _ = _gpu_counts(*synth.bipartite_random(200, 300, 0.2, seed))
+        assert t == 0 and k == 0
+    for kk in (3, 4, 5, 50, 1000):
+        t, k, _ = _gpu_counts(*synth.wheel(kk))
+        assert t == (4 if kk == 3 else kk) and k == (1 if kk == 3 else 0)
+
+
+# -------------------------------------------------------------------- random graphs --
+@pytest.mark.parametrize("seed", range(40))
+def test_random_er(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 600))
+    p = float(rng.choice([0.002, 0.01, 0.05, 0.2]))
+    _check(*synth.er(n, p, seed))
+
+
+@pytest.mark.parametrize("scale,ef,seed", [(s, ef, seed) for s in (6, 8, 10, 12, 14) for ef in (4, 16)
+                                           for seed in range(4)])
+def test_random_rmat(scale, ef, seed):
+    _check(*synth.rmat(scale, ef, 1000 * scale + 10 * ef + seed))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_multigraph_with_noise(seed):
+    src, dst = synth.random_graph(int(np.random.default_rng(seed).integers(3, 3000)), 20000, seed)
+    _check(src, dst)
+
+
+# ---------------------------------------------------------------------- edge cases --
+def test_empty_and_degenerate():
+    e = np.zeros(0, np.uint32)
+    assert _gpu_counts(e, e)[:2] == (0, 0)
+    loops = np.arange(100, dtype=np.uint32)
+    assert _gpu_counts(loops, loops)[:2] == (0, 0)
+    assert _gpu_counts(np.array([5], np.uint32), np.array([9], np.uint32))[:2] == (0, 0)
+    tri = (np.array([0, 1, 2], np.uint32), np.array([1, 2, 0], np.uint32))
+    assert _gpu_counts(*tri)[:2] == (1, 0)
+
+
+def test_ids_near_u32_max_dictionary_path():
+    rng = np.random.default_rng(3)
+    src, dst = synth.rmat(11, 8, 77)
+    ids = np.unique(np.concatenate([src, dst]))
+    new = rng.choice(2**32 - 1, size=ids.size, replace=False).astype(np.uint64)
+    new[-1] = 2**32 - 1
+    s = new[np.searchsorted(ids, src)].astype(np.uint32)
+    d = new[np.searchsorted(ids, dst)].astype(np.uint32)
+    assert _check(s, d) == _check(src, dst)
+
+
+def test_huge_star_and_hub():
+    s, d = synth.star(200_000)
+    assert _gpu_counts(s, d)[:2] == (0, 0)
+    # star plus a path over the leaves: every path edge closes one triangle with the hub
+    leaves = np.arange(1, 200_001, dtype=np.uint32)
+    s = np.concatenate([s, leaves[:-1]])
+    d = np.concatenate([d, leaves[1:]])
+    assert _gpu_counts(s, d, k4=True)[:2] == (199_999, 0)
+
+
+# ------------------------------------------------------------------ invariances (T5/T6) --
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True),
+                                dict(min_bitset_card=1), dict(bin_small_max=2**32 - 1),
+                                dict(bin_small_max=1, bin_large_min=1), dict(bin_small_max=1, bin_large_min=2**32 - 1),
+                                dict(torch_allocator=True)])
+def test_layout_and_binning_invariance(kw):
+    src, dst = synth.rmat(13, 16, 5)
+    base = _gpu_counts(src, dst)[:2]
+    assert _gpu_counts(src, dst, **kw)[:2] == base
+
+
+def test_device_input_and_stream():
+    import torch
+    src, dst = synth.rmat(12, 16, 6)
+    ts = torch.from_numpy(src.view(np.int32)).cuda()
+    td = torch.from_numpy(dst.view(np.int32)).cuda()
+    st = torch.cuda.Stream()
+    with eh.Graph(ts, td, stream=st) as g:
+        t = g.count_triangles()
+    assert t == oracle.count_triangles(src, dst)
+
+
+# ----------------------------------------------------------------------- ingest (T4) --
+@pytest.mark.parametrize("seed", range(3))
+def test_ingest_csr_matches_oracle(seed):
+    src, dst = synth.rmat(12, 16, 40 + seed)
+    with eh.Graph(src, dst) as g:
+        row_ptr, col, orig, isb = g.export()
+    og = oracle.Graph(src, dst)
+    vid, deg, off, adj = og.export()
+    n = vid.size
+    assert orig.size == n and row_ptr[-1] == og.m
+    # rank order = ascending (degree, original id)
+    pos = np.searchsorted(vid, orig)
+    assert np.array_equal(vid[pos], orig)
+    key = deg[pos].astype(np.int64) * 2**32 + orig
+    assert np.all(np.diff(key) > 0)
+    for r in range(n):
+        lst = col[row_ptr[r]:row_ptr[r + 1]]
+        assert np.all(np.diff(lst.astype(np.int64)) > 0) and (lst.size == 0 or lst[0] > r)
+        i = pos[r]
+        assert np.array_equal(np.sort(orig[lst]), adj[off[i]:off[i + 1]])
+
+
+# ---------------------------------------------------------------- configs C1..C4 --
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_config_small(name):
+    cfg = synth.CONFIGS[name]
+    _check(*cfg.generate(), k4=(name == "C2"))
+
+
+def test_config_c3_triangles():
+    src, dst = synth.CONFIGS["C3"].generate()
+    t, _, st = _gpu_counts(src, dst, k4=False)
+    assert t == oracle.count_triangles(src, dst)
+
+
+def test_config_c4_4cliques():
+    src, dst = synth.CONFIGS["C4"].generate()
+    with eh.Graph(src, dst) as g:
+        k = g.count_4cliques()
+    assert k == oracle.count_4cliques(src, dst) and k > 2**32
+
+
+# ----------------------------------------------------------------------- intersect --
+def test_intersect_golden(golden_dir):
+    w = json.load(open(os.path.join(golden_dir, "w3_intersect.json")))
+    for c in w["cases"]:
+        b = list(range(0, 256)) if c["b"] == "range(0,256)" else c["b"]
+        assert eh.intersect(np.array(c["a"], np.uint32), np.array(b, np.uint32)).tolist() == c["out"]
+
+
+def test_intersect_random_vs_numpy():
+    rng = np.random.default_rng(1)
+    for t in range(1500):
+        na, nb = (int(v) for v in rng.integers(0, 2000, 2))
+        if t % 7 == 0:
+            nb = int(rng.integers(0, 200000))
+        hi = int(rng.choice([64, 4096, 2**20, 2**32]))
+        a = np.unique(rng.integers(0, hi, na, dtype=np.uint64)).astype(np.uint32)
+        b = np.unique(rng.integers(0, hi, nb, dtype=np.uint64)).astype(np.uint32)
+        got = eh.intersect(a, b)
+        np.testing.assert_array_equal(got, np.intersect1d(a, b))
+        assert eh.intersect(b, a, count_only=True) == got.size
+
+
+def test_intersect_device_and_errors():
+    import torch
+    a = torch.arange(0, 1000, 3, dtype=torch.int32, device="cuda")
+    b = torch.arange(0, 1000, 5, dtype=torch.int32, device="cuda")
+    out = eh.intersect(a, b)
+    assert out.is_cuda and out.cpu().tolist() == list(range(0, 1000, 15))
+    with pytest.raises(eh.EHError) as ei:
+        eh.intersect(np.array([3, 2], np.uint32), np.array([1], np.uint32))
+    assert ei.value.status == eh.EH_EUNSORTED
+    with pytest.raises(eh.EHError):
+        eh.intersect(np.array([2, 2], np.uint32), np.array([1], np.uint32))
