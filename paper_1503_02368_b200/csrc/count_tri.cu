@@ -1,16 +1,32 @@
-// count_tri.cu -- SURVEY.md §8(a) rows a8 (triangle Generic-Join) and a10
-// (warp-shuffle uint64 reduction).
+// count_tri.cu -- SURVEY.md §8(a) rows a7 (work classes), a8 (triangle
+// Generic-Join) and a10 (warp-shuffle uint64 reduction).
 //
 // Loop nest with R = S = T = E+ in rank space:
 //     for x:  for y in N+(x):  Q += | N+(y) cap N+(x) |
-// Because N+(y) lies above y, only the suffix A = N+(x) after y can match,
-// so the intersection is |A cap N+(y)|.
-// Dispatch on the layout pair:
-//   N+(y) bitset         -> probe each a in A into the bitset (uint cap bitset)
-//   N+(y) uint, |A|<=|B| -> each a in A binary-searches B   (galloping side)
-//   N+(y) uint, |A|>|B|  -> each b in B binary-searches A    (staged in smem)
-// COUNT(*) is accumulated per lane in u64, reduced with __shfl_xor_sync and
-// added once per warp with atomicAdd(unsigned long long*).
+// Every element of N+(y) is larger than y, so |N+(y) cap N+(x)| equals
+// |N+(y) cap A| with A = N+(x) after y: a
+// membership test against the WHOLE of N+(x) is exact, and a loop over A only
+// needs the suffix.
+//
+// Each edge (x, y) picks the cheapest intersection for its layout pair
+// (min property):
+//   PROBE  N+(y) bitset: every a in A tests its bit in y's bitset (uint cap
+//          bitset).  In the warp kernel these probes are
+//          flattened over all such rows of x so that all 32 lanes work even
+//          when |A| < 32.
+//   AND    N+(y) bitset and x staged as a bitmap in shared memory: AND the
+//          overlapping 128-bit chunks and popcount (bitset cap bitset,
+//          PAPER.md:636) when the overlap is small relative to |A|.
+//   STREAM N+(y) uint: lanes stream y's list with coalesced 128-bit loads and
+//          test each element against N+(x) staged in shared memory -- as an
+//          exact bitmap over x's span when it fits, else as an open-addressing
+//          hash table (O(1) per element; a B200 replacement for the paper's
+//          SIMD shuffling merge, same result).
+//   SEARCH N+(y) uint and |A| log|B| << |B|: each a in A binary-searches B
+//          (the galloping side of the uint hybrid).
+// Work classes (a7): 2 <= |N+(x)| <= kWarpMaxD run one warp per x, larger x one
+// CTA per x with warps over rows.  COUNT(*) is a per-lane u64, reduced with
+// __shfl_xor_sync, one atomicAdd(unsigned long long) per warp.
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "sets.cuh"
@@ -19,46 +35,254 @@ namespace eh {
 
 namespace {
 
-constexpr int kTriWarps = 8;
-constexpr int kTriBlock = kTriWarps * 32;
-constexpr int kXCap = 1024;  // N+(x) staged in shared memory when |N+(x)| <= kXCap
+// ------------------------------------------------------------ tunables --
+constexpr int kWarpMaxD = 128;        // warp kernel handles 2 <= d <= kWarpMaxD
+constexpr int kWarpBmWords = 512;     // warp-kernel x structure: 2 KB (bitmap of 16384 ids or 512-slot hash)
+constexpr int kWK_Warps = 8;
+constexpr int kCtaWarps = 16;
+constexpr int kCtaXCap = 4096;        // CTA kernel stages N+(x) in smem up to this size
+constexpr int kCtaBmWords = 16384;    // CTA-kernel x structure: 64 KB (bitmap of 524288 ids or hash)
+constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor * |A| + 8
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
-__global__ void __launch_bounds__(kTriBlock) k_tri_warp(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
-                                                        const uint32_t* __restrict__ bs,
-                                                        const uint32_t* __restrict__ work, uint64_t nwork,
-                                                        unsigned long long* __restrict__ ctr) {
-  __shared__ __align__(16) uint32_t xs_s[kTriWarps][kXCap];
+enum RowKind : uint8_t { kSkip = 0, kProbe = 1, kAnd = 2, kStream = 3, kSearchGlobal = 4 };
+enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2 };
+
+struct YInfo {
+  uint32_t list;  // col offset of N+(y) in 16-B units
+  uint32_t len;   // |N+(y)|
+  uint32_t pool;  // bitset pool offset of chunk c0 in 16-B chunks (if bitset)
+  uint32_t c0;    // first chunk
+  uint32_t c1;    // one past last chunk (c1 == c0: no bitset)
+};
+
+__device__ __forceinline__ YInfo yinfo(const uint4* __restrict__ desc, uint32_t y) {
+  const uint4 d = __ldg(desc + y);
+  const uint32_t z1 = __ldg(&desc[y + 1].z);
+  return YInfo{d.x, d.y, d.z, d.w, d.w + (z1 - d.z)};
+}
+
+__device__ __forceinline__ uint32_t probe_bits(const uint32_t* __restrict__ bs, const YInfo& y, uint32_t e) {
+  const uint32_t c = e >> 7;
+  if (c < y.c0 || c >= y.c1) return 0u;
+  return (__ldg(bs + (uint64_t)y.pool * 4 + ((e >> 5) - 4u * y.c0)) >> (e & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t gmem_search(const uint32_t* __restrict__ a, uint32_t n, uint32_t e) {
+  uint32_t lo = 0, len = n;
+  while (len > 0) {
+    const uint32_t h = len >> 1;
+    if (__ldg(a + lo + h) < e) { lo += h + 1; len -= h + 1; } else { len = h; }
+  }
+  return (lo < n && __ldg(a + lo) == e) ? 1u : 0u;
+}
+
+// ---------------------------------------------- x's membership structure --
+// N+(x) in shared memory as (a) an exact bitmap over [lo, lo + nbits), (b) an
+// open-addressing hash table with 2^hbits slots (load <= 1/4), or (c) the
+// sorted list itself (binary search; CTA kernel only when |N+(x)| > kCtaXCap).
+struct XSet {
+  uint32_t* tab;        // bitmap words or hash slots (shared memory)
+  const uint32_t* xs;   // sorted N+(x) (shared or global)
+  uint32_t mode, lo, nbits, hshift, hmask, d, amin, amax;
+
+  __device__ __forceinline__ uint32_t contains(uint32_t e) const {
+    if (mode == kBitmap) {
+      const uint32_t o = e - lo;
+      return (o < nbits) ? (tab[o >> 5] >> (o & 31)) & 1u : 0u;
+    }
+    if (e < amin || e > amax) return 0u;
+    if (mode == kHash) {
+      uint32_t s = (e * 2654435761u) >> hshift;
+      for (;;) {
+        const uint32_t v = tab[s];
+        if (v == e) return 1u;
+        if (v == kEmpty) return 0u;
+        s = (s + 1) & hmask;
+      }
+    }
+    uint32_t lo2 = 0, len = d;
+    while (len > 0) {
+      const uint32_t h = len >> 1;
+      if (xs[lo2 + h] < e) { lo2 += h + 1; len -= h + 1; } else { len = h; }
+    }
+    return (lo2 < d && xs[lo2] == e) ? 1u : 0u;
+  }
+};
+
+// Build the structure cooperatively (tid in [0, nthreads)); caller syncs afterwards.
+__device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, const uint32_t* xs, uint32_t d,
+                                           int tid, int nthreads) {
+  XSet s;
+  s.tab = tab;
+  s.xs = xs;
+  s.d = d;
+  s.amin = xs[0];
+  s.amax = xs[d - 1];
+  const uint32_t lo = (s.amin >> 7) << 7;
+  const uint64_t span_bits = (uint64_t)(((s.amax >> 7) + 1) << 7) - lo;
+  uint32_t hbits = 5;
+  while ((1u << hbits) < 4 * d) ++hbits;
+  if (span_bits <= 32ull * tab_words) {
+    s.mode = kBitmap;
+    s.lo = lo;
+    s.nbits = (uint32_t)span_bits;
+    s.hshift = s.hmask = 0;
+    for (uint32_t k = tid; k < s.nbits / 32; k += nthreads) tab[k] = 0u;
+  } else if ((1u << hbits) <= tab_words) {
+    s.mode = kHash;
+    s.lo = s.nbits = 0;
+    s.hshift = 32 - hbits;
+    s.hmask = (1u << hbits) - 1u;
+    for (uint32_t k = tid; k < (1u << hbits); k += nthreads) tab[k] = kEmpty;
+  } else {
+    s.mode = kSorted;
+    s.lo = s.nbits = s.hshift = s.hmask = 0;
+  }
+  if (nthreads == 32) __syncwarp(); else __syncthreads();
+  if (s.mode == kBitmap) {
+    for (uint32_t k = tid; k < d; k += nthreads) {
+      const uint32_t o = xs[k] - lo;
+      atomicOr(&tab[o >> 5], 1u << (o & 31));
+    }
+  } else if (s.mode == kHash) {
+    for (uint32_t k = tid; k < d; k += nthreads) {
+      const uint32_t e = xs[k];
+      uint32_t h = (e * 2654435761u) >> s.hshift;
+      while (atomicCAS(&tab[h], kEmpty, e) != kEmpty) h = (h + 1) & s.hmask;
+    }
+  }
+  return s;
+}
+
+// Decide the intersection for row i of x (y = xs[i], |A| = a).
+__device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XSet& X) {
+  if (a == 0 || y.len == 0) return kSkip;
+  if (y.c1 > y.c0) {
+    if (X.mode == kBitmap) {
+      const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
+      const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
+      if (hi <= lo) return kSkip;
+      if (hi - lo <= kAndFactor * a + 8) return kAnd;
+    }
+    return kProbe;
+  }
+  const uint32_t lg = 32 - __clz(y.len);
+  if ((uint64_t)a * lg * 4 < y.len) return kSearchGlobal;
+  return kStream;
+}
+
+// ---- warp-level row bodies (all 32 lanes; return this lane's partial count) --
+__device__ __forceinline__ uint32_t row_and(const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X, int lane) {
+  const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
+  const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
+  uint32_t c = 0;
+  const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
+  const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
+  for (uint32_t k = lo + lane; k < hi; k += 32) {                 // k: absolute chunk index
+    const uint4 u = __ldg(yb + (k - y.c0));
+    const uint4 v = xb[k - xc0];
+    c += __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint32_t row_stream(const uint32_t* __restrict__ col, const YInfo& y, const XSet& X,
+                                               int lane) {
+  uint32_t c = 0;
+  const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
+  const uint32_t nfull = y.len >> 2;
+  for (uint32_t k = lane; k < nfull; k += 32) {
+    const uint4 v = __ldg(yl + k);
+    c += X.contains(v.x) + X.contains(v.y) + X.contains(v.z) + X.contains(v.w);
+  }
+  if (lane < (y.len & 3)) c += X.contains(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + lane));
+  return c;
+}
+
+__device__ __forceinline__ uint32_t row_search_global(const uint32_t* __restrict__ col, const YInfo& y,
+                                                      const uint32_t* A, uint32_t na, int lane) {
+  uint32_t c = 0;
+  for (uint32_t j = lane; j < na; j += 32) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
+  return c;
+}
+
+// ------------------------------------------------------------ warp kernel --
+struct WarpSmem {
+  uint32_t xs[kWarpMaxD];
+  uint32_t tab[kWarpBmWords];
+  YInfo yi[kWarpMaxD];
+  uint8_t kind[kWarpMaxD];
+  uint8_t prow[kWarpMaxD];  // rows of kind kProbe, in order
+};
+
+__global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __restrict__ desc,
+                                                             const uint32_t* __restrict__ col,
+                                                             const uint32_t* __restrict__ bs,
+                                                             const uint32_t* __restrict__ work, uint64_t nwork,
+                                                             unsigned long long* __restrict__ ctr) {
+  __shared__ __align__(16) WarpSmem sm_all[kWK_Warps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = sm_all[w];
+  const unsigned lt = (1u << lane) - 1u;
   unsigned long long cnt = 0;
   for (;;) {
     unsigned long long wi = 0;
     if (lane == 0) wi = atomicAdd(&ctr[1], 1ull);
     wi = __shfl_sync(kFull, wi, 0);
     if (wi >= nwork) break;
-    const uint32_t x = work[wi];
-    const uint4 dx = desc[x];
-    const uint32_t d = dx.y;
+    const uint32_t x = __ldg(work + wi);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;  // 2 <= d <= kWarpMaxD
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
-    const uint32_t* xs = xg;
-    if (d <= kXCap) {
-      const uint4* src4 = reinterpret_cast<const uint4*>(xg);
-      uint4* dst4 = reinterpret_cast<uint4*>(xs_s[w]);
-      for (uint32_t k = lane; k < (d + 3) / 4; k += 32) dst4[k] = __ldg(src4 + k);
-      __syncwarp();
-      xs = xs_s[w];
-    }
-    for (uint32_t i = 0; i + 1 < d; ++i) {
-      const uint32_t y = xs[i];
-      const SetRef sy = set_of(desc, col, bs, y);
-      if (sy.len == 0) continue;
-      const uint32_t a0 = i + 1, na = d - a0;
-      if (sy.bits) {
-        for (uint32_t j = a0 + lane; j < d; j += 32) cnt += bit_probe(sy, xs[j]);
-      } else if (na <= sy.len) {
-        for (uint32_t j = a0 + lane; j < d; j += 32) cnt += search_probe(sy.list, sy.len, xs[j]);
-      } else {
-        for (uint32_t k = lane; k < sy.len; k += 32) cnt += search_probe_any(xs + a0, na, __ldg(sy.list + k));
+    for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
+      reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
+    __syncwarp();
+    const XSet X = build_xset(sm.tab, kWarpBmWords, sm.xs, d, lane, 32);
+    // row preparation: lanes over rows
+    uint32_t nprobe = 0;
+    for (uint32_t i0 = 0; i0 + 1 < d; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint8_t kd = kSkip;
+      if (i + 1 < d) {
+        const YInfo y = yinfo(desc, sm.xs[i]);
+        kd = row_kind(y, d - 1 - i, X);
+        sm.yi[i] = y;
+        sm.kind[i] = kd;
       }
+      const unsigned pm = __ballot_sync(kFull, kd == kProbe);
+      if (kd == kProbe) sm.prow[nprobe + __popc(pm & lt)] = (uint8_t)i;
+      nprobe += __popc(pm);
+    }
+    __syncwarp();
+    // flattened probes: each lane walks (row r, column j) with stride 32
+    if (nprobe) {
+      uint32_t r = 0, i = sm.prow[0], j = i + 1 + lane;
+      while (j >= d) {
+        const uint32_t over = j - d;
+        if (++r >= nprobe) break;
+        i = sm.prow[r];
+        j = i + 1 + over;
+      }
+      while (r < nprobe) {
+        cnt += probe_bits(bs, sm.yi[i], sm.xs[j]);
+        j += 32;
+        while (j >= d) {
+          const uint32_t over = j - d;
+          if (++r >= nprobe) break;
+          i = sm.prow[r];
+          j = i + 1 + over;
+        }
+      }
+    }
+    // remaining rows, one at a time, lanes cooperating
+    for (uint32_t i = 0; i + 1 < d; ++i) {
+      const uint8_t kd = sm.kind[i];
+      if (kd <= kProbe) continue;
+      const YInfo y = sm.yi[i];
+      if (kd == kAnd) cnt += row_and(bs, y, X, lane);
+      else if (kd == kStream) cnt += row_stream(col, y, X, lane);
+      else cnt += row_search_global(col, y, sm.xs + i + 1, d - 1 - i, lane);
     }
     __syncwarp();
   }
@@ -66,20 +290,90 @@ __global__ void __launch_bounds__(kTriBlock) k_tri_warp(const uint4* __restrict_
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
+// ------------------------------------------------------------- CTA kernel --
+__global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
+                                                            const uint32_t* __restrict__ col,
+                                                            const uint32_t* __restrict__ bs,
+                                                            const uint32_t* __restrict__ work, uint64_t nwork,
+                                                            unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) uint32_t dsm[];
+  uint32_t* xs_s = dsm;             // kCtaXCap
+  uint32_t* tab = dsm + kCtaXCap;   // kCtaBmWords
+  __shared__ unsigned long long s_wi;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long cnt = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
+    __syncthreads();
+    const unsigned long long wi = s_wi;
+    if (wi >= nwork) break;
+    const uint32_t x = __ldg(work + wi);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;
+    const uint32_t* xg = col + (uint64_t)dx.x * 4;
+    const uint32_t* xs = xg;
+    if (d <= (uint32_t)kCtaXCap) {
+      for (uint32_t k = threadIdx.x; k < (d + 3) / 4; k += blockDim.x)
+        reinterpret_cast<uint4*>(xs_s)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
+      xs = xs_s;
+    }
+    __syncthreads();
+    const XSet X = build_xset(tab, (d <= (uint32_t)kCtaXCap) ? kCtaBmWords : 0, xs, d, threadIdx.x, blockDim.x);
+    __syncthreads();
+    // rows round-robin over warps (row i has |A| = d-1-i, so the loads even out);
+    // the descriptor of the next row is fetched before the current one is processed
+    uint32_t i = w;
+    YInfo y = (i + 1 < d) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
+    while (i + 1 < d) {
+      const uint32_t inext = i + kCtaWarps;
+      const YInfo ynext = (inext + 1 < d) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
+      const uint32_t na = d - 1 - i;
+      const uint8_t kd = row_kind(y, na, X);
+      const uint32_t* A = xs + i + 1;
+      if (kd == kProbe) {
+        for (uint32_t j = lane; j < na; j += 32) cnt += probe_bits(bs, y, A[j]);
+      } else if (kd == kAnd) {
+        cnt += row_and(bs, y, X, lane);
+      } else if (kd == kStream) {
+        cnt += row_stream(col, y, X, lane);
+      } else if (kd == kSearchGlobal) {
+        cnt += row_search_global(col, y, A, na, lane);
+      }
+      i = inext;
+      y = ynext;
+    }
+    __syncthreads();
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
+}
+
+constexpr size_t kCtaSmem = (size_t)(kCtaXCap + kCtaBmWords) * 4;
+
 }  // namespace
 
 uint64_t count_triangles(eh_graph* g) {
   cudaStream_t s = g->stream;
-  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 2 * sizeof(unsigned long long), s));
-  const uint64_t nwork = g->n_work[0] + g->n_work[1] + g->n_work[2];
-  if (nwork) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((nwork + kTriWarps - 1) / kTriWarps, (uint64_t)kSMs * 8);
-    k_tri_warp<<<grid, kTriBlock, 0, s>>>(g->desc, g->col, g->bs, g->work, nwork, g->d_counter);
+  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
+  // work classes 0 and 1 (d <= kWarpMaxD) -> warp kernel; class 2 -> CTA kernel
+  const uint64_t nsmall = g->n_work[0] + g->n_work[1];
+  const uint64_t nlarge = g->n_work[2];
+  if (nlarge) {
+    EH_CUDA(cudaFuncSetAttribute(k_tri_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmem));
+    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * 2);
+    k_tri_cta<<<grid, kCtaWarps * 32, kCtaSmem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter);
+    EH_LAUNCH("k_tri_cta");
+  }
+  if (nsmall) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps, (uint64_t)kSMs * 8);
+    k_tri_warp<<<grid, kWK_Warps * 32, 0, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
     EH_LAUNCH("k_tri_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   return g->h_counter[0];
 }
+
+uint32_t tri_warp_max_degree() { return kWarpMaxD; }
 
 }  // namespace eh

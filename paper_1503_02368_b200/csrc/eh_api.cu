@@ -46,7 +46,6 @@ void destroy(eh_graph* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (void* p : g->owned) g->alloc.release(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
-  if (g->h_counter) cudaFreeHost(g->h_counter);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete g;
@@ -103,8 +102,16 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       g->alloc.hook_free = c.dev_free;
       g->alloc.ctx = c.alloc_ctx;
       g->alloc.stream = g->stream;
-      EH_CUDA(cudaMallocHost(&g->h_counter, 2 * sizeof(unsigned long long)));
-      g->d_counter = (unsigned long long*)g->own(2 * sizeof(unsigned long long));
+      if (!c.dev_alloc) {
+        // keep freed blocks in the stream-ordered pool instead of returning them to
+        // the driver at every synchronisation (re-mapping costs ~100 ms per load)
+        cudaMemPool_t pool;
+        EH_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        EH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      }
+      eh::PhaseTimer timer(g->stream);
+      g->d_counter = (unsigned long long*)g->own(4 * sizeof(unsigned long long));
       // a1: upload (borrowed inputs are copied)
       eh::DBuf<uint32_t> in;
       const uint32_t* d_src = src;
@@ -116,11 +123,15 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
         d_src = in.p;
         d_dst = in.p + n;
       }
-      eh::build_trie(g, d_src, d_dst, n);
+      timer.mark("upload");
+      eh::build_trie(g, d_src, d_dst, n, &timer);
       in.reset();
       eh::build_layouts(g);
+      timer.mark("layouts");
       eh::build_worklists(g);
+      timer.mark("worklists");
       EH_CUDA(cudaStreamSynchronize(g->stream));
+      timer.report("eh_load_edges");
     } catch (...) {
       destroy(g);
       throw;

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -130,6 +131,40 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key
 uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s);
 
+// Optional phase timing (EH_TIMING=1 in the environment): CUDA events between
+// phases, reported on stderr.  Development aid; off by default.
+struct PhaseTimer {
+  cudaStream_t s;
+  bool on;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  explicit PhaseTimer(cudaStream_t st) : s(st) {
+    const char* e = getenv("EH_TIMING");
+    on = e && e[0] == '1';
+    mark("start");
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  void report(const char* what) {
+    if (!on || ev.size() < 2) return;
+    cudaEventSynchronize(ev.back().second);
+    fprintf(stderr, "[eh timing] %s:", what);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, " %s=%.3fms", ev[i].first, ms);
+    }
+    fprintf(stderr, "\n");
+  }
+  ~PhaseTimer() {
+    for (auto& p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 template <typename T>
 inline T read_scalar(const T* d, cudaStream_t s) {
   T h;
@@ -164,7 +199,7 @@ struct eh_graph {
   uint32_t* work = nullptr;
   uint64_t n_work[3] = {0, 0, 0};
   unsigned long long* d_counter = nullptr;  // 2 x u64 accumulators
-  unsigned long long* h_counter = nullptr;  // pinned host mirror
+  unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
 
   std::vector<void*> owned;  // every device allocation above
   uint64_t device_bytes = 0;
@@ -179,12 +214,13 @@ struct eh_graph {
 
 namespace eh {
 // ingest.cu: canonicalise, sort, dedup, degree rank, orient, CSR; fills g->desc/col/orig_id.
-void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n);
+void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, PhaseTimer* t = nullptr);
 // trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
 void build_layouts(eh_graph* g);
 void build_worklists(eh_graph* g);
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);
+uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept
 uint64_t count_4cliques(eh_graph* g);
 // intersect.cu
 int64_t intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);

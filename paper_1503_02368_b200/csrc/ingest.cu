@@ -154,7 +154,8 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* 
 
 }  // namespace
 
-void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n) {
+void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, PhaseTimer* tm) {
+  auto mark = [&](const char* p) { if (tm) tm->mark(p); };
   Allocator& al = g->alloc;
   cudaStream_t s = g->stream;
   const unsigned TB = 256;
@@ -202,13 +203,16 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   EH_LAUNCH("k_canon");
   msrc.reset();
   mdst.reset();
+  mark("canon");
   uint64_t* sk = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);
+  mark("sort1");
   uint64_t* other = (sk == keys.p) ? alt.p : keys.p;
 
   // ---- a3: dedup (unique adjacent keys, sentinel dropped) -> m distinct undirected edges
   const uint64_t m = select_if(n, UniqueKeyPred{sk, sentinel}, CopyKeyEmit{sk, other}, al, s);
   uint64_t* ukeys = other;
   g->m = m;
+  mark("dedup");
 
   // ---- a4: degree + (degree, id) rank
   DBuf<uint32_t> deg(al, n_ids);
@@ -236,6 +240,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   }
   rkeys.reset();
   ralt.reset();
+  mark("degree_rank");
 
   // ---- a5: orient + CSR (padded to 16 B per list)
   const uint32_t rb = std::max<uint32_t>(1, bitlen(n_act ? n_act - 1 : 0));
@@ -248,7 +253,9 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
     EH_LAUNCH("k_orient");
   }
   deg.reset();
+  mark("orient");
   uint64_t* osorted = radix_sort_u64(okeys, oalt_buf.p, m, 2 * rb, al, s);
+  mark("sort2");
   // offsets: unpadded row starts and padded 16-B offsets
   DBuf<uint64_t> row_start(al, n_act + 1), off16(al, n_act + 1), tot(al, 2);
   DBuf<uint32_t> p4(al, std::max<uint64_t>(1, n_act));
@@ -272,6 +279,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   k_max_u32<<<grid_for(n_act, TB * 8), TB, 0, s>>>(dplus.p, n_act, dmax.p);
   EH_LAUNCH("k_max_u32");
   g->max_dplus = read_scalar(dmax.p, s);
+  mark("csr");
 }
 
 }  // namespace eh

@@ -150,8 +150,12 @@ void build_worklists(eh_graph* g) {
   Allocator& al = g->alloc;
   cudaStream_t s = g->stream;
   const uint64_t n = g->n_act;
+  // classes 0/1 run the warp-per-x kernels, class 2 the CTA-per-x kernels; the
+  // warp kernels stage N+(x) in a fixed shared-memory slot, so d above their
+  // capacity always lands in class 2 whatever the configuration asks for.
+  const uint64_t cap = (uint64_t)tri_warp_max_degree() + 1;
   const uint64_t small_max = g->bin_small_max ? g->bin_small_max : 32;
-  const uint64_t large_min = g->bin_large_min ? g->bin_large_min : 4096;
+  const uint64_t large_min = std::min<uint64_t>(g->bin_large_min ? g->bin_large_min : cap, cap);
   g->work = (uint32_t*)g->own(std::max<uint64_t>(1, n) * 4);
   uint64_t lo[3], hi[3];  // class c holds lo[c] <= d < hi[c]
   lo[0] = 2;

@@ -1,0 +1,28 @@
+"""Profiling driver (development aid): load one config, then call the count
+entry point `--reps` times.  Run under ncu with -k regex:k_tri / k_k4."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import synth  # noqa: E402
+import paper_1503_02368_b200 as eh  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C3")
+ap.add_argument("--query", default="tri", choices=["tri", "k4"])
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--tau", type=int, default=0)
+ap.add_argument("--small", type=int, default=0)
+ap.add_argument("--large", type=int, default=0)
+a = ap.parse_args()
+src, dst = synth.CONFIGS[a.config].generate()
+with eh.Graph(src, dst, tau=a.tau, bin_small_max=a.small, bin_large_min=a.large) as g:
+    st = g.stats()
+    for _ in range(a.reps):
+        t0 = time.perf_counter()
+        c = g.count_triangles() if a.query == "tri" else g.count_4cliques()
+        print(f"{a.query} = {c}  {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
+    print(st, flush=True)
