@@ -8,25 +8,27 @@
 // membership test against the WHOLE of N+(x) is exact, and a loop over A only
 // needs the suffix.
 //
-// Each edge (x, y) picks the cheapest intersection for its layout pair
-// (min property):
+// Each edge (x, y) -- a "row" of x -- picks the cheapest intersection for its
+// layout pair (min property):
 //   PROBE  N+(y) bitset: every a in A tests its bit in y's bitset (uint cap
-//          bitset).  In the warp kernel these probes are
-//          flattened over all such rows of x so that all 32 lanes work even
-//          when |A| < 32.
+//          bitset).
 //   AND    N+(y) bitset and x staged as a bitmap in shared memory: AND the
 //          overlapping 128-bit chunks and popcount (bitset cap bitset,
 //          PAPER.md:636) when the overlap is small relative to |A|.
-//   STREAM N+(y) uint: lanes stream y's list with coalesced 128-bit loads and
-//          test each element against N+(x) staged in shared memory -- as an
-//          exact bitmap over x's span when it fits, else as an open-addressing
-//          hash table (O(1) per element; a B200 replacement for the paper's
-//          SIMD shuffling merge, same result).
+//   STREAM N+(y) uint: stream y's list with coalesced 128-bit loads and test
+//          each element against N+(x) staged in shared memory -- an exact
+//          bitmap over x's span when it fits, else an open-addressing hash
+//          table (O(1) per element; a B200 replacement for the paper's SIMD
+//          shuffling merge, same result).
 //   SEARCH N+(y) uint and |A| log|B| << |B|: each a in A binary-searches B
 //          (the galloping side of the uint hybrid).
-// Work classes (a7): 2 <= |N+(x)| <= kWarpMaxD run one warp per x, larger x one
-// CTA per x with warps over rows.  COUNT(*) is a per-lane u64, reduced with
-// __shfl_xor_sync, one atomicAdd(unsigned long long) per warp.
+// Rows are short (tens of units), so each row runs on an 8-lane sub-warp
+// group: 4 rows in flight per warp, and 8 lanes x 16 B still read one full
+// 128-B line per load.  Work classes (a7): 2 <= |N+(x)| <= kWarpMaxD run one
+// warp per x (rows ordered by kind so the 4 groups of a warp rarely diverge);
+// larger x run one CTA per x (64 groups over rows).  COUNT(*) is a per-lane
+// u64, reduced with __shfl_xor_sync, one atomicAdd(unsigned long long) per warp
+// (PAPER.md:243).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "sets.cuh"
@@ -36,6 +38,7 @@ namespace eh {
 namespace {
 
 // ------------------------------------------------------------ tunables --
+constexpr int kG = 8;                 // lanes per row group
 constexpr int kWarpMaxD = 128;        // warp kernel handles 2 <= d <= kWarpMaxD
 constexpr int kWarpBmWords = 512;     // warp-kernel x structure: 2 KB (bitmap of 16384 ids or 512-slot hash)
 constexpr int kWK_Warps = 8;
@@ -172,48 +175,57 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
   return kStream;
 }
 
-// ---- warp-level row bodies (all 32 lanes; return this lane's partial count) --
-__device__ __forceinline__ uint32_t row_and(const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X, int lane) {
-  const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
-  const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
-  uint32_t c = 0;
-  const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
-  const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
-  for (uint32_t k = lo + lane; k < hi; k += 32) {                 // k: absolute chunk index
-    const uint4 u = __ldg(yb + (k - y.c0));
-    const uint4 v = xb[k - xc0];
-    c += __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
-  }
-  return c;
+// ---- group-level row bodies: kG lanes, gl = lane within the group --------
+__device__ __forceinline__ uint32_t and4(const uint4 u, const uint4 v) {
+  return __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
 }
 
-__device__ __forceinline__ uint32_t row_stream(const uint32_t* __restrict__ col, const YInfo& y, const XSet& X,
-                                               int lane) {
+__device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restrict__ col,
+                                            const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X,
+                                            const uint32_t* A, uint32_t na, uint32_t gl) {
   uint32_t c = 0;
-  const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
-  const uint32_t nfull = y.len >> 2;
-  for (uint32_t k = lane; k < nfull; k += 32) {
-    const uint4 v = __ldg(yl + k);
-    c += X.contains(v.x) + X.contains(v.y) + X.contains(v.z) + X.contains(v.w);
+  if (kd == kProbe) {
+    for (uint32_t j = gl; j < na; j += kG) c += probe_bits(bs, y, A[j]);
+  } else if (kd == kAnd) {
+    const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
+    const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
+    const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
+    const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
+    uint32_t k = lo + gl;                                            // absolute chunk index
+    for (; k + kG < hi; k += 2 * kG) {
+      const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + kG - y.c0));
+      c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + kG - xc0]);
+    }
+    if (k < hi) c += and4(__ldg(yb + (k - y.c0)), xb[k - xc0]);
+  } else if (kd == kStream) {
+    const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
+    const uint32_t nfull = y.len >> 2;
+    uint32_t k = gl;
+    for (; k + kG < nfull; k += 2 * kG) {
+      const uint4 v0 = __ldg(yl + k), v1 = __ldg(yl + k + kG);
+      c += X.contains(v0.x) + X.contains(v0.y) + X.contains(v0.z) + X.contains(v0.w);
+      c += X.contains(v1.x) + X.contains(v1.y) + X.contains(v1.z) + X.contains(v1.w);
+    }
+    if (k < nfull) {
+      const uint4 v = __ldg(yl + k);
+      c += X.contains(v.x) + X.contains(v.y) + X.contains(v.z) + X.contains(v.w);
+    }
+    if (gl < (y.len & 3)) c += X.contains(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + gl));
+  } else if (kd == kSearchGlobal) {
+    for (uint32_t j = gl; j < na; j += kG) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
   }
-  if (lane < (y.len & 3)) c += X.contains(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + lane));
-  return c;
-}
-
-__device__ __forceinline__ uint32_t row_search_global(const uint32_t* __restrict__ col, const YInfo& y,
-                                                      const uint32_t* A, uint32_t na, int lane) {
-  uint32_t c = 0;
-  for (uint32_t j = lane; j < na; j += 32) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
   return c;
 }
 
 // ------------------------------------------------------------ warp kernel --
-struct WarpSmem {
+// One warp per x with 2 <= |N+(x)| <= kWarpMaxD.  Lanes classify the rows in
+// parallel, rows are ordered by kind, then the 4 groups take rows round-robin.
+struct __align__(16) WarpSmem {
   uint32_t xs[kWarpMaxD];
   uint32_t tab[kWarpBmWords];
   YInfo yi[kWarpMaxD];
   uint8_t kind[kWarpMaxD];
-  uint8_t prow[kWarpMaxD];  // rows of kind kProbe, in order
+  uint8_t ord[kWarpMaxD];  // non-skip rows grouped by kind
 };
 
 __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __restrict__ desc,
@@ -221,8 +233,10 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
                                                              const uint32_t* __restrict__ bs,
                                                              const uint32_t* __restrict__ work, uint64_t nwork,
                                                              unsigned long long* __restrict__ ctr) {
-  __shared__ __align__(16) WarpSmem sm_all[kWK_Warps];
+  extern __shared__ __align__(16) uint32_t dsm_w[];
+  WarpSmem* sm_all = reinterpret_cast<WarpSmem*>(dsm_w);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t grp = lane / kG, gl = lane % kG;
   WarpSmem& sm = sm_all[w];
   const unsigned lt = (1u << lane) - 1u;
   unsigned long long cnt = 0;
@@ -239,50 +253,29 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
     __syncwarp();
     const XSet X = build_xset(sm.tab, kWarpBmWords, sm.xs, d, lane, 32);
-    // row preparation: lanes over rows
-    uint32_t nprobe = 0;
-    for (uint32_t i0 = 0; i0 + 1 < d; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      uint8_t kd = kSkip;
-      if (i + 1 < d) {
-        const YInfo y = yinfo(desc, sm.xs[i]);
-        kd = row_kind(y, d - 1 - i, X);
-        sm.yi[i] = y;
-        sm.kind[i] = kd;
-      }
-      const unsigned pm = __ballot_sync(kFull, kd == kProbe);
-      if (kd == kProbe) sm.prow[nprobe + __popc(pm & lt)] = (uint8_t)i;
-      nprobe += __popc(pm);
+    const uint32_t nrows = d - 1;
+    for (uint32_t i = lane; i < nrows; i += 32) {
+      const YInfo y = yinfo(desc, sm.xs[i]);
+      sm.yi[i] = y;
+      sm.kind[i] = row_kind(y, nrows - i, X);
     }
     __syncwarp();
-    // flattened probes: each lane walks (row r, column j) with stride 32
-    if (nprobe) {
-      uint32_t r = 0, i = sm.prow[0], j = i + 1 + lane;
-      while (j >= d) {
-        const uint32_t over = j - d;
-        if (++r >= nprobe) break;
-        i = sm.prow[r];
-        j = i + 1 + over;
-      }
-      while (r < nprobe) {
-        cnt += probe_bits(bs, sm.yi[i], sm.xs[j]);
-        j += 32;
-        while (j >= d) {
-          const uint32_t over = j - d;
-          if (++r >= nprobe) break;
-          i = sm.prow[r];
-          j = i + 1 + over;
-        }
+    uint32_t nr = 0;
+#pragma unroll
+    for (int kdi = 0; kdi < 4; ++kdi) {
+      const uint8_t want = (uint8_t)(kProbe + kdi);
+      for (uint32_t i0 = 0; i0 < nrows; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool sel = i < nrows && sm.kind[i] == want;
+        const unsigned m = __ballot_sync(kFull, sel);
+        if (sel) sm.ord[nr + __popc(m & lt)] = (uint8_t)i;
+        nr += __popc(m);
       }
     }
-    // remaining rows, one at a time, lanes cooperating
-    for (uint32_t i = 0; i + 1 < d; ++i) {
-      const uint8_t kd = sm.kind[i];
-      if (kd <= kProbe) continue;
-      const YInfo y = sm.yi[i];
-      if (kd == kAnd) cnt += row_and(bs, y, X, lane);
-      else if (kd == kStream) cnt += row_stream(col, y, X, lane);
-      else cnt += row_search_global(col, y, sm.xs + i + 1, d - 1 - i, lane);
+    __syncwarp();
+    for (uint32_t r = grp; r < nr; r += 32 / kG) {
+      const uint32_t i = sm.ord[r];
+      cnt += grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -291,6 +284,9 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
 }
 
 // ------------------------------------------------------------- CTA kernel --
+// One CTA per x with |N+(x)| > kWarpMaxD; its 64 groups take rows round-robin
+// (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
+// descriptor before working on the current one.
 __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -300,7 +296,9 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
   uint32_t* xs_s = dsm;             // kCtaXCap
   uint32_t* tab = dsm + kCtaXCap;   // kCtaBmWords
   __shared__ unsigned long long s_wi;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gid = threadIdx.x / kG, gl = threadIdx.x % kG;
   unsigned long long cnt = 0;
   for (;;) {
     if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
@@ -320,25 +318,14 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
     __syncthreads();
     const XSet X = build_xset(tab, (d <= (uint32_t)kCtaXCap) ? kCtaBmWords : 0, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
-    // rows round-robin over warps (row i has |A| = d-1-i, so the loads even out);
-    // the descriptor of the next row is fetched before the current one is processed
-    uint32_t i = w;
-    YInfo y = (i + 1 < d) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
-    while (i + 1 < d) {
-      const uint32_t inext = i + kCtaWarps;
-      const YInfo ynext = (inext + 1 < d) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      const uint32_t na = d - 1 - i;
-      const uint8_t kd = row_kind(y, na, X);
-      const uint32_t* A = xs + i + 1;
-      if (kd == kProbe) {
-        for (uint32_t j = lane; j < na; j += 32) cnt += probe_bits(bs, y, A[j]);
-      } else if (kd == kAnd) {
-        cnt += row_and(bs, y, X, lane);
-      } else if (kd == kStream) {
-        cnt += row_stream(col, y, X, lane);
-      } else if (kd == kSearchGlobal) {
-        cnt += row_search_global(col, y, A, na, lane);
-      }
+    const uint32_t nrows = d - 1;
+    uint32_t i = gid;
+    YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
+    while (i < nrows) {
+      const uint32_t inext = i + kGroups;
+      const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
+      const uint32_t na = nrows - i;
+      cnt += grp_row(row_kind(y, na, X), col, bs, y, X, xs + i + 1, na, gl);
       i = inext;
       y = ynext;
     }
@@ -366,7 +353,9 @@ uint64_t count_triangles(eh_graph* g) {
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps, (uint64_t)kSMs * 8);
-    k_tri_warp<<<grid, kWK_Warps * 32, 0, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    const size_t smem = sizeof(WarpSmem) * kWK_Warps;
+    EH_CUDA(cudaFuncSetAttribute(k_tri_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tri_warp<<<grid, kWK_Warps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
     EH_LAUNCH("k_tri_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
