@@ -54,7 +54,8 @@ enum {
 typedef struct {
   /* Set-level layout optimizer: a set S becomes a bitset iff
    * span(S) = max - min + 1 < bitset_tau * |S| (strict; u64 arithmetic).
-   * 0 -> 32 (reading c10; the paper's AVX register is tau = 256). */
+   * 0 -> 128 (tuned on B200, reading c10; the paper's AVX register
+   * is tau = 256).  Counts do not depend on tau. */
   uint32_t bitset_tau;
   int32_t device; /* CUDA ordinal, honoured only with EH_SET_DEVICE */
   void* stream;   /* cudaStream_t used for all work; NULL -> a library-owned stream */

@@ -88,7 +88,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
     try {
       g->device = dev;
       g->flags = c.flags;
-      g->tau = c.bitset_tau ? c.bitset_tau : 32;
+      g->tau = c.bitset_tau ? c.bitset_tau : 128;
       g->min_bitset_card = c.min_bitset_card ? c.min_bitset_card : 2;
       g->bin_small_max = c.bin_small_max;
       g->bin_large_min = c.bin_large_min;
@@ -112,6 +112,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       }
       eh::PhaseTimer timer(g->stream);
       g->d_counter = (unsigned long long*)g->own(4 * sizeof(unsigned long long));
+      timer.mark("alloc");
       // a1: upload (borrowed inputs are copied)
       eh::DBuf<uint32_t> in;
       const uint32_t* d_src = src;

@@ -137,6 +137,12 @@ struct PhaseTimer {
   cudaStream_t s;
   bool on;
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  std::vector<double> host_ms;
+  static double now_ms() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
   explicit PhaseTimer(cudaStream_t st) : s(st) {
     const char* e = getenv("EH_TIMING");
     on = e && e[0] == '1';
@@ -148,15 +154,16 @@ struct PhaseTimer {
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
     ev.emplace_back(name, e);
+    host_ms.push_back(now_ms());
   }
   void report(const char* what) {
     if (!on || ev.size() < 2) return;
     cudaEventSynchronize(ev.back().second);
-    fprintf(stderr, "[eh timing] %s:", what);
+    fprintf(stderr, "[eh timing] %s (gpu ms / host ms at mark):", what);
     for (size_t i = 1; i < ev.size(); ++i) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-      fprintf(stderr, " %s=%.3fms", ev[i].first, ms);
+      fprintf(stderr, " %s=%.3f/%.3f", ev[i].first, ms, host_ms[i] - host_ms[i - 1]);
     }
     fprintf(stderr, "\n");
   }

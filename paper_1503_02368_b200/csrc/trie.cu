@@ -30,8 +30,10 @@ __global__ void k_layout(const uint4* __restrict__ desc, const uint32_t* __restr
       if (!all_uint && d.y >= min_card && span < (uint64_t)tau * d.y) {
         c0 = first >> 7;
         nc = (last >> 7) - c0 + 1;
-        by = 4u * ((last >> 5) - (first >> 5) + 1);  // words spanned
       }
+      // B_tri's bytes(S) is defined at tau = 32 whatever layout the kernels use
+      // (SURVEY.md §8(d)): words spanned for a tau=32 bitset, else 4|S|.
+      if (span < 32ull * d.y) by = 4u * ((last >> 5) - (first >> 5) + 1);
     }
     nchunks[v] = nc;
     chunk0[v] = c0;
