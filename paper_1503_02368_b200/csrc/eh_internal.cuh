@@ -127,6 +127,9 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 // Returns the buffer holding the result (keys or alt).
 uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s);
+// Sort segment v = data[off16[v]*4 .. + len[v]) in place for v < nseg (segsort.cu).
+void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
+                        Allocator& al, cudaStream_t s);
 // Same for u32 keys.
 uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s);

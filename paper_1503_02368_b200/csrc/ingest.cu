@@ -106,33 +106,34 @@ __global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint
   }
 }
 
-// a5: orient low rank -> high rank; key (lo << rb) | hi; out-degree histogram.
+// a5: orient low rank -> high rank: out-degree histogram of the low end.
 __global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint32_t* __restrict__ rank,
-                         uint32_t rb, uint64_t* __restrict__ okeys, uint32_t* __restrict__ dplus) {
+                         uint32_t* __restrict__ dplus) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint32_t ru = rank[k >> b], rv = rank[k & mask];
+    atomicAdd(&dplus[min(ru, rv)], 1u);
+  }
+}
+
+// a5: counting-sort scatter of the high end into the low end's padded list
+// (slot order within a list is arbitrary; segmented_sort_u32 orders it).
+__global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b,
+                              const uint32_t* __restrict__ rank, const uint64_t* __restrict__ off16,
+                              uint32_t* __restrict__ cursor, uint32_t* __restrict__ col) {
   const uint64_t mask = (1ull << b) - 1ull;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[i];
     const uint32_t ru = rank[k >> b], rv = rank[k & mask];
     const uint32_t lo = min(ru, rv), hi = max(ru, rv);
-    okeys[i] = ((uint64_t)lo << rb) | hi;
-    atomicAdd(&dplus[lo], 1u);
+    col[off16[lo] * 4 + atomicAdd(&cursor[lo], 1u)] = hi;
   }
 }
 
 __global__ void k_pad4(const uint32_t* __restrict__ d, uint64_t n, uint32_t* __restrict__ p4) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     p4[i] = (d[i] + 3u) >> 2;
-}
-
-__global__ void k_fill_col(const uint64_t* __restrict__ okeys, uint64_t m, uint32_t rb,
-                           const uint64_t* __restrict__ row_start, const uint64_t* __restrict__ off16,
-                           uint32_t* __restrict__ col) {
-  const uint64_t mask = (1ull << rb) - 1ull;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = okeys[i];
-    const uint64_t lo = k >> rb;
-    col[off16[lo] * 4 + (i - row_start[lo])] = (uint32_t)(k & mask);
-  }
 }
 
 __global__ void k_desc_base(const uint64_t* __restrict__ off16, const uint32_t* __restrict__ dplus, uint64_t n_act,
@@ -243,42 +244,41 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   mark("degree_rank");
 
   // ---- a5: orient + CSR (padded to 16 B per list)
-  const uint32_t rb = std::max<uint32_t>(1, bitlen(n_act ? n_act - 1 : 0));
+  // out-degree of the low end, padded 16-B list offsets, counting-sort scatter
+  // of the high end, then each list sorted in on-chip memory (segsort.cu).
   DBuf<uint32_t> dplus(al, std::max<uint64_t>(1, n_act));
   EH_CUDA(cudaMemsetAsync(dplus.p, 0, std::max<uint64_t>(1, n_act) * 4, s));
-  uint64_t* okeys = sk;  // sk is free once dedup copied the unique keys into `other`
-  DBuf<uint64_t> oalt_buf(al, std::max<uint64_t>(1, m));
   if (m) {
-    k_orient<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, rb, okeys, dplus.p);
+    k_orient<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, dplus.p);
     EH_LAUNCH("k_orient");
   }
-  deg.reset();
-  mark("orient");
-  uint64_t* osorted = radix_sort_u64(okeys, oalt_buf.p, m, 2 * rb, al, s);
-  mark("sort2");
-  // offsets: unpadded row starts and padded 16-B offsets
-  DBuf<uint64_t> row_start(al, n_act + 1), off16(al, n_act + 1), tot(al, 2);
+  DBuf<uint64_t> off16(al, n_act + 1), tot(al, 1);
   DBuf<uint32_t> p4(al, std::max<uint64_t>(1, n_act));
-  scan_exclusive_u32(dplus.p, row_start.p, n_act, tot.p, al, s);
   k_pad4<<<grid_for(n_act, TB * 4), TB, 0, s>>>(dplus.p, n_act, p4.p);
   EH_LAUNCH("k_pad4");
-  scan_exclusive_u32(p4.p, off16.p, n_act, tot.p + 1, al, s);
-  const uint64_t total16 = read_scalar(tot.p + 1, s);
+  scan_exclusive_u32(p4.p, off16.p, n_act, tot.p, al, s);
+  const uint64_t total16 = read_scalar(tot.p, s);
   if (total16 >= (1ull << 32)) fail(EH_EINVAL, "graph too large: %llu padded 16-B list blocks", (unsigned long long)total16);
   g->col_elems = total16 * 4;
   g->col = (uint32_t*)g->own(std::max<uint64_t>(16, total16 * 16));
   EH_CUDA(cudaMemsetAsync(g->col, 0xFF, std::max<uint64_t>(16, total16 * 16), s));
+  mark("orient");
   if (m) {
-    k_fill_col<<<grid_for(m, TB * 4), TB, 0, s>>>(osorted, m, rb, row_start.p, off16.p, g->col);
-    EH_LAUNCH("k_fill_col");
+    EH_CUDA(cudaMemsetAsync(p4.p, 0, std::max<uint64_t>(1, n_act) * 4, s));  // reuse as cursors
+    k_scatter_col<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, off16.p, p4.p, g->col);
+    EH_LAUNCH("k_scatter_col");
   }
-  g->desc = (uint4*)g->own((n_act + 1) * sizeof(uint4));
-  k_desc_base<<<grid_for(n_act + 1, TB * 4), TB, 0, s>>>(off16.p, dplus.p, n_act, total16, g->desc);
-  EH_LAUNCH("k_desc_base");
+  deg.reset();
   EH_CUDA(cudaMemsetAsync(dmax.p, 0, 4, s));
   k_max_u32<<<grid_for(n_act, TB * 8), TB, 0, s>>>(dplus.p, n_act, dmax.p);
   EH_LAUNCH("k_max_u32");
   g->max_dplus = read_scalar(dmax.p, s);
+  mark("scatter");
+  segmented_sort_u32(g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s);
+  mark("segsort");
+  g->desc = (uint4*)g->own((n_act + 1) * sizeof(uint4));
+  k_desc_base<<<grid_for(n_act + 1, TB * 4), TB, 0, s>>>(off16.p, dplus.p, n_act, total16, g->desc);
+  EH_LAUNCH("k_desc_base");
   mark("csr");
 }
 

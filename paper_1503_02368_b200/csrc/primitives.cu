@@ -1,12 +1,22 @@
-// primitives.cu -- device-wide scan and LSD radix sort (hand-written, sm_100a).
+// primitives.cu -- device-wide scan and one-sweep LSD radix sort (hand-written, sm_100a).
 //
-// Used by ingest (SURVEY.md §8(a) rows a2-a5: "hand-written radix sort, dedup",
-// CSR offsets) and by the layout/work-list builders.  Radix sort is the classic
-// reduce-then-scan LSD scheme: per pass (i) every CTA histograms the digit over
-// its contiguous key range, (ii) one exclusive scan of the digit-major
-// [256 x CTAs] table gives every (digit, CTA) its global base, (iii) every CTA
-// re-reads its range tile by tile, ranks keys stably inside each warp with
-// __match_any_sync and scatters them.  Stable, deterministic, no look-back.
+// Used by ingest (SURVEY.md §8(a) rows a2-a4: "hand-written radix sort, dedup",
+// the (degree, id) rank sort, dictionary encoding) and by the layout / work-list
+// builders.
+//
+// Radix sort = one-sweep LSD with 8-bit digits:
+//   (1) one read of the keys builds the digit histograms of EVERY pass;
+//       an exclusive scan per pass gives each digit's global base;
+//   (2) per pass, tiles of 4096 keys are taken in launch order from an atomic
+//       tile counter; each tile ranks its keys stably (warp sub-tiles in order,
+//       __match_any_sync within a round of 32), publishes its per-digit counts,
+//       and finds its per-digit exclusive prefix by decoupled look-back over the
+//       preceding tiles (status = {flag:2, value:62} in one 64-bit word, so flag
+//       and value are published atomically).  Keys are reordered by digit in
+//       shared memory and written out in digit runs (coalesced).
+// One read + one write of the keys per pass; forward progress holds because a
+// tile only waits on tiles that obtained a smaller index, i.e. started earlier.
+// Passes whose digit is constant over all keys are skipped.
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 
@@ -85,100 +95,157 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 }
 
 // ------------------------------------------------------------- radix sort --
-constexpr int kRadixBlock = 256;
-constexpr int kRadixWarps = kRadixBlock / 32;
-constexpr int kRadixItems = 8;                       // keys per lane per tile
-constexpr int kRadixTile = kRadixBlock * kRadixItems;  // 2048 keys
-constexpr int kRadixDigits = 256;
+constexpr int kRBlock = 256;
+constexpr int kRWarps = kRBlock / 32;
+constexpr int kRItems = 16;                   // keys per lane per tile
+constexpr int kRTile = kRBlock * kRItems;     // 4096 keys
+constexpr int kRDigits = 256;
+constexpr int kRMaxPasses = 8;
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
+// (1) all-pass digit histograms in one read
 template <typename K>
-__global__ void __launch_bounds__(kRadixBlock) k_radix_upsweep(const K* __restrict__ keys, uint64_t n,
-                                                               uint64_t per_cta, uint32_t shift,
-                                                               uint64_t* __restrict__ hist) {
-  __shared__ uint32_t h[kRadixDigits];
-  for (int i = threadIdx.x; i < kRadixDigits; i += kRadixBlock) h[i] = 0;
+__global__ void __launch_bounds__(kRBlock) k_radix_hist(const K* __restrict__ keys, uint64_t n, uint32_t passes,
+                                                        unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t h[kRMaxPasses][kRDigits];
+  for (int i = threadIdx.x; i < kRMaxPasses * kRDigits; i += kRBlock) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint64_t b = (uint64_t)blockIdx.x * per_cta;
-  const uint64_t e = min(n, b + per_cta);
-  for (uint64_t i = b + threadIdx.x; i < e; i += kRadixBlock) {
-    const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xFFu;
-    atomicAdd(&h[d], 1u);
+  for (uint64_t i = (uint64_t)blockIdx.x * kRBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kRBlock) {
+    const K k = keys[i];
+    for (uint32_t p = 0; p < passes; ++p) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 0xFFu], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) hist[(uint64_t)d * gridDim.x + blockIdx.x] = h[d];
+  for (int i = threadIdx.x; i < (int)passes * kRDigits; i += kRBlock) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(&hist[i], (unsigned long long)c);
+  }
 }
 
+// per-pass exclusive scan of the 256 digit counts (one CTA of 256 threads per pass)
+__global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long long* __restrict__ hist,
+                                                         unsigned long long* __restrict__ base,
+                                                         uint32_t* __restrict__ trivial, uint64_t n) {
+  __shared__ unsigned long long sw[kRDigits / 32 + 1];
+  const uint32_t p = blockIdx.x;
+  const unsigned long long c = hist[p * kRDigits + threadIdx.x];
+  unsigned long long tot;
+  const unsigned long long ex = block_exclusive_scan<kRDigits>(c, sw, &tot);
+  base[p * kRDigits + threadIdx.x] = ex;
+  if (c == n) trivial[p] = 1u;  // every key has this digit: the pass is the identity
+}
+
+// (2) one pass
 template <typename K>
-__global__ void __launch_bounds__(kRadixBlock) k_radix_downsweep(const K* __restrict__ keys, K* __restrict__ out,
-                                                                 uint64_t n, uint64_t per_cta, uint32_t shift,
-                                                                 const uint64_t* __restrict__ offs) {
-  __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];  // per-warp digit counts, then exclusive prefixes
-  __shared__ uint32_t ttot[kRadixDigits];               // per-tile digit totals
-  __shared__ uint64_t cbase[kRadixDigits];              // global output base of each digit for this tile
+__global__ void __launch_bounds__(kRBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+                                                        uint32_t shift, const unsigned long long* __restrict__ base,
+                                                        unsigned long long* __restrict__ status,
+                                                        uint32_t* __restrict__ tile_ctr) {
+  __shared__ __align__(16) K skeys[kRTile];
+  __shared__ uint32_t wcnt[kRWarps][kRDigits];
+  __shared__ uint32_t tdp[kRDigits];          // tile-local exclusive digit prefix
+  __shared__ unsigned long long goff[kRDigits];  // global position of the tile's first key with digit d
+  __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) cbase[d] = offs[(uint64_t)d * gridDim.x + blockIdx.x];
-  for (int i = threadIdx.x; i < kRadixWarps * kRadixDigits; i += kRadixBlock) (&wcnt[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  for (int i = threadIdx.x; i < kRWarps * kRDigits; i += kRBlock) (&wcnt[0][0])[i] = 0;
   __syncthreads();
-  const uint64_t b = (uint64_t)blockIdx.x * per_cta;
-  const uint64_t e = min(n, b + per_cta);
+  const uint64_t tile = s_tile;
+  const uint64_t t0 = tile * kRTile;
+  const uint64_t tn = min((uint64_t)kRTile, n - t0);
   const unsigned lt = (1u << lane) - 1u;
-  for (uint64_t t0 = b; t0 < e; t0 += kRadixTile) {
-    K key[kRadixItems];
-    uint32_t rk[kRadixItems], dg[kRadixItems];
-    // warp w owns the contiguous sub-tile [t0 + w*32*ITEMS, +32*ITEMS), read in rounds of 32:
-    // ranking rounds in order and lanes by position keeps the sort stable.
+  K key[kRItems];
+  uint32_t rk[kRItems], dg[kRItems];
 #pragma unroll
-    for (int r = 0; r < kRadixItems; ++r) {
-      const uint64_t idx = t0 + (uint64_t)w * 32 * kRadixItems + (uint64_t)r * 32 + lane;
-      const bool valid = idx < e;
-      key[r] = valid ? keys[idx] : K(0);
-      const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 0xFFu) : 0x100u;
-      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-      const uint32_t before = (d < 0x100u) ? wcnt[w][d] : 0u;
-      __syncwarp();
-      if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = before + __popc(peers);
-      __syncwarp();
-      rk[r] = before + __popc(peers & lt);
-      dg[r] = d;
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) {
-      uint32_t run = 0;
+  for (int r = 0; r < kRItems; ++r) {
+    const uint32_t li = (uint32_t)w * 32 * kRItems + (uint32_t)r * 32 + lane;
+    const bool valid = li < tn;
+    key[r] = valid ? in[t0 + li] : K(0);
+    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 0xFFu) : 0x100u;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const uint32_t before = (d < 0x100u) ? wcnt[w][d] : 0u;
+    __syncwarp();
+    if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = before + __popc(peers);
+    __syncwarp();
+    rk[r] = before + __popc(peers & lt);
+    dg[r] = d;
+  }
+  __syncthreads();
+  // thread d: per-warp exclusive prefix, tile total, tile-local digit prefix
+  const uint32_t d = threadIdx.x;
+  uint32_t run = 0;
 #pragma unroll
-      for (int ww = 0; ww < kRadixWarps; ++ww) {
-        const uint32_t c = wcnt[ww][d];
-        wcnt[ww][d] = run;
-        run += c;
+  for (int ww = 0; ww < kRWarps; ++ww) {
+    const uint32_t c = wcnt[ww][d];
+    wcnt[ww][d] = run;
+    run += c;
+  }
+  const uint32_t total = run;
+  {
+    unsigned long long* my = status + tile * kRDigits + d;
+    if (tile == 0) {
+      __stcg(my, kFlagInc | total);
+      goff[d] = base[d];
+    } else {
+      __stcg(my, kFlagAgg | total);
+      unsigned long long excl = 0;
+      uint64_t t = tile - 1;
+      for (;;) {
+        const unsigned long long sv = *((volatile unsigned long long*)(status + t * kRDigits + d));
+        const unsigned long long fl = sv & ~kValMask;
+        if (fl == 0) continue;  // predecessor has not published yet (it started before us)
+        excl += sv & kValMask;
+        if (fl == kFlagInc) break;
+        --t;
       }
-      ttot[d] = run;
+      __stcg(my, kFlagInc | (excl + total));
+      goff[d] = base[d] + excl;
     }
-    __syncthreads();
+  }
+  // tile-local exclusive prefix over digits
+  {
+    __shared__ uint32_t sw[kRDigits / 32 + 1];
+    uint32_t tt;
+    tdp[d] = block_exclusive_scan<kRBlock>(total, sw, &tt);
+  }
+  __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kRadixItems; ++r)
-      if (dg[r] < 0x100u) out[cbase[dg[r]] + wcnt[w][dg[r]] + rk[r]] = key[r];
-    __syncthreads();
-    for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) cbase[d] += ttot[d];
-    for (int i = threadIdx.x; i < kRadixWarps * kRadixDigits; i += kRadixBlock) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
+  for (int r = 0; r < kRItems; ++r)
+    if (dg[r] < 0x100u) skeys[tdp[dg[r]] + wcnt[w][dg[r]] + rk[r]] = key[r];
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tn; i += kRBlock) {
+    const K k = skeys[i];
+    const uint32_t dd = (uint32_t)(k >> shift) & 0xFFu;
+    out[goff[dd] + (i - tdp[dd])] = k;
   }
 }
 
 template <typename K>
 static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& al, cudaStream_t s) {
   if (n <= 1 || key_bits == 0) return keys;
-  const uint64_t tiles = (n + kRadixTile - 1) / kRadixTile;
-  const unsigned G = (unsigned)std::min<uint64_t>(tiles, (uint64_t)kSMs * 8);
-  const uint64_t per_cta = ((tiles + G - 1) / G) * kRadixTile;
-  const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
-  DBuf<uint64_t> hist(al, (size_t)kRadixDigits * grid);
+  const uint32_t passes = (key_bits + 7) / 8;
+  DBuf<unsigned long long> hist(al, (size_t)passes * kRDigits), base(al, (size_t)passes * kRDigits);
+  DBuf<uint32_t> trivial(al, kRMaxPasses), ctr(al, kRMaxPasses);
+  EH_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes(), s));
+  EH_CUDA(cudaMemsetAsync(trivial.p, 0, trivial.bytes(), s));
+  EH_CUDA(cudaMemsetAsync(ctr.p, 0, ctr.bytes(), s));
+  k_radix_hist<K><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, n, passes, hist.p);
+  EH_LAUNCH("k_radix_hist");
+  k_radix_base<<<passes, kRDigits, 0, s>>>(hist.p, base.p, trivial.p, n);
+  EH_LAUNCH("k_radix_base");
+  uint32_t triv[kRMaxPasses];
+  EH_CUDA(cudaMemcpyAsync(triv, trivial.p, sizeof triv, cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  const uint64_t tiles = (n + kRTile - 1) / kRTile;
+  if (tiles >= (1ull << 31)) fail(EH_EINVAL, "radix sort: too many keys");
+  DBuf<unsigned long long> status(al, (size_t)tiles * kRDigits);
   K* src = keys;
   K* dst = alt;
-  for (uint32_t shift = 0; shift < key_bits; shift += 8) {
-    k_radix_upsweep<K><<<grid, kRadixBlock, 0, s>>>(src, n, per_cta, shift, hist.p);
-    EH_LAUNCH("k_radix_upsweep");
-    scan_exclusive_u64(hist.p, hist.p, (uint64_t)kRadixDigits * grid, nullptr, al, s);
-    k_radix_downsweep<K><<<grid, kRadixBlock, 0, s>>>(src, dst, n, per_cta, shift, hist.p);
-    EH_LAUNCH("k_radix_downsweep");
+  for (uint32_t p = 0; p < passes; ++p) {
+    if (triv[p]) continue;
+    EH_CUDA(cudaMemsetAsync(status.p, 0, status.bytes(), s));
+    k_radix_pass<K><<<(unsigned)tiles, kRBlock, 0, s>>>(src, dst, n, 8 * p, base.p + (size_t)p * kRDigits, status.p,
+                                                       ctr.p + p);
+    EH_LAUNCH("k_radix_pass");
     K* t = src; src = dst; dst = t;
   }
   return src;

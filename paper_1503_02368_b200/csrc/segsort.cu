@@ -1,0 +1,183 @@
+// segsort.cu -- sort many short u32 segments in place (SURVEY.md §8(a) row a5:
+// "CSR with strictly increasing out-lists").
+//
+// After orientation the out-lists are filled by a counting-sort scatter (atomic
+// cursor per list), which leaves each list in arbitrary order.  Degree
+// orientation bounds every list: |N+(x)| <= sqrt(2m) (each out-neighbour has
+// degree >= deg(x) >= |N+(x)|), so lists are short and sort in on-chip memory:
+//   len <= 32          one warp, bitonic network in registers (__shfl_xor_sync)
+//   33 .. 1024         one warp, bitonic network in shared memory
+//   1025 .. 8192       one CTA, bitonic network in shared memory
+//   longer (rare)      gathered as (segment << 32 | value) keys and sorted by the
+//                      device-wide LSD radix sort, then scattered back.
+#include "eh_internal.cuh"
+#include "primitives.cuh"
+
+#include <algorithm>
+
+namespace eh {
+
+namespace {
+
+constexpr uint32_t kPad = 0xFFFFFFFFu;
+constexpr int kMidMax = 1024, kMidWarps = 8;
+constexpr int kBigMax = 8192, kBigThreads = 1024;
+
+struct Seg {
+  const uint64_t* off16;  // segment v starts at element off16[v] * 4
+  const uint32_t* len;
+};
+
+__global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t t = warp; t < nids; t += nw) {
+    const uint32_t v = ids[t];
+    const uint32_t n = sg.len[v];
+    uint32_t* p = data + sg.off16[v] * 4;
+    uint32_t x = (lane < (int)n) ? p[lane] : kPad;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(kFull, x, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        x = (lower == up) ? min(x, o) : max(x, o);
+      }
+    }
+    if (lane < (int)n) p[lane] = x;
+  }
+}
+
+// Bitonic sort of s[0..N) (N power of two) by `nt` cooperating threads.
+template <bool kCta>
+__device__ __forceinline__ void bitonic_smem(uint32_t* s, uint32_t N, uint32_t tid, uint32_t nt) {
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = tid; t < N / 2; t += nt) {
+        const uint32_t i = 2 * t - (t & (j - 1));
+        const uint32_t l = i + j;
+        const bool asc = (i & k) == 0;
+        const uint32_t a = s[i], b = s[l];
+        if ((a > b) == asc) { s[i] = b; s[l] = a; }
+      }
+      if (kCta) __syncthreads(); else __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMidWarps * 32) k_seg_mid(uint32_t* __restrict__ data, Seg sg,
+                                                              const uint32_t* __restrict__ ids, uint64_t nids) {
+  __shared__ uint32_t sm[kMidWarps][kMidMax];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t warp = (uint64_t)blockIdx.x * kMidWarps + w;
+  const uint64_t nw = (uint64_t)gridDim.x * kMidWarps;
+  uint32_t* s = sm[w];
+  for (uint64_t t = warp; t < nids; t += nw) {
+    const uint32_t v = ids[t];
+    const uint32_t n = sg.len[v];
+    uint32_t* p = data + sg.off16[v] * 4;
+    uint32_t N = 64;
+    while (N < n) N <<= 1;
+    for (uint32_t i = lane; i < N; i += 32) s[i] = (i < n) ? p[i] : kPad;
+    __syncwarp();
+    bitonic_smem<false>(s, N, lane, 32);
+    for (uint32_t i = lane; i < n; i += 32) p[i] = s[i];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_seg_big(uint32_t* __restrict__ data, Seg sg,
+                                                          const uint32_t* __restrict__ ids, uint64_t nids) {
+  __shared__ uint32_t s[kBigMax];
+  for (uint64_t t = blockIdx.x; t < nids; t += gridDim.x) {
+    const uint32_t v = ids[t];
+    const uint32_t n = sg.len[v];
+    uint32_t* p = data + sg.off16[v] * 4;
+    uint32_t N = 2048;
+    while (N < n) N <<= 1;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? p[i] : kPad;
+    __syncthreads();
+    bitonic_smem<true>(s, N, threadIdx.x, blockDim.x);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = s[i];
+    __syncthreads();
+  }
+}
+
+// ---- fallback for segments longer than kBigMax ----
+__global__ void k_seg_gather(const uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids,
+                             uint64_t nids, const uint64_t* __restrict__ goff, uint64_t* __restrict__ keys) {
+  for (uint64_t t = blockIdx.x; t < nids; t += gridDim.x) {
+    const uint32_t v = ids[t];
+    const uint32_t n = sg.len[v];
+    const uint32_t* p = data + sg.off16[v] * 4;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[goff[t] + i] = (t << 32) | p[i];
+  }
+}
+__global__ void k_seg_scatter(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids,
+                              uint64_t nids, const uint64_t* __restrict__ goff, const uint64_t* __restrict__ keys) {
+  for (uint64_t t = blockIdx.x; t < nids; t += gridDim.x) {
+    const uint32_t v = ids[t];
+    const uint32_t n = sg.len[v];
+    uint32_t* p = data + sg.off16[v] * 4;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = (uint32_t)keys[goff[t] + i];
+  }
+}
+
+struct LenPred {
+  const uint32_t* len;
+  uint32_t lo, hi;  // lo <= len <= hi
+  __device__ bool operator()(uint64_t v) const { const uint32_t n = len[v]; return n >= lo && n <= hi; }
+};
+struct IdEmit {
+  uint32_t* out;
+  __device__ void operator()(uint64_t pos, uint64_t v) const { out[pos] = (uint32_t)v; }
+};
+__global__ void k_gather_len(const uint32_t* __restrict__ len, const uint32_t* __restrict__ ids, uint64_t n,
+                             uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = len[ids[i]];
+}
+
+}  // namespace
+
+void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
+                        Allocator& al, cudaStream_t s) {
+  if (nseg == 0 || max_len <= 1) return;
+  const Seg sg{off16, len};
+  DBuf<uint32_t> ids(al, nseg);
+  const uint32_t bounds[4][2] = {{2, 32}, {33, (uint32_t)kMidMax}, {(uint32_t)kMidMax + 1, (uint32_t)kBigMax},
+                                 {(uint32_t)kBigMax + 1, 0xFFFFFFFFu}};
+  for (int tier = 0; tier < 4; ++tier) {
+    if (max_len < bounds[tier][0]) break;
+    const uint64_t k = select_if(nseg, LenPred{len, bounds[tier][0], bounds[tier][1]}, IdEmit{ids.p}, al, s);
+    if (k == 0) continue;
+    if (tier == 0) {
+      k_seg_small<<<grid_for(k * 32, 256), 256, 0, s>>>(data, sg, ids.p, k);
+      EH_LAUNCH("k_seg_small");
+    } else if (tier == 1) {
+      k_seg_mid<<<grid_for(k, kMidWarps), kMidWarps * 32, 0, s>>>(data, sg, ids.p, k);
+      EH_LAUNCH("k_seg_mid");
+    } else if (tier == 2) {
+      k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, ids.p, k);
+      EH_LAUNCH("k_seg_big");
+    } else {
+      DBuf<uint32_t> lens(al, k);
+      DBuf<uint64_t> goff(al, k), tot(al, 1);
+      k_gather_len<<<grid_for(k, 256), 256, 0, s>>>(len, ids.p, k, lens.p);
+      EH_LAUNCH("k_gather_len");
+      scan_exclusive_u32(lens.p, goff.p, k, tot.p, al, s);
+      const uint64_t total = read_scalar(tot.p, s);
+      DBuf<uint64_t> keys(al, total), alt(al, total);
+      const unsigned g = (unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 4);
+      k_seg_gather<<<g, 512, 0, s>>>(data, sg, ids.p, k, goff.p, keys.p);
+      EH_LAUNCH("k_seg_gather");
+      uint64_t* sorted = radix_sort_u64(keys.p, alt.p, total, 32 + bitlen(k - 1), al, s);
+      k_seg_scatter<<<g, 512, 0, s>>>(data, sg, ids.p, k, goff.p, sorted);
+      EH_LAUNCH("k_seg_scatter");
+    }
+  }
+}
+
+}  // namespace eh
