@@ -76,12 +76,30 @@ struct CopyU32Emit {
 };
 
 // a4: degree = number of distinct neighbours.
+// Keys are sorted by the low end u, so u-side counts are run lengths inside a
+// warp (one atomic per run); v-side atomics are aggregated over equal v in the
+// warp (hubs would otherwise serialise thousands of atomics on one address).
 __global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint32_t* __restrict__ deg) {
   const uint64_t mask = (1ull << b) - 1ull;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    atomicAdd(&deg[k >> b], 1u);
-    atomicAdd(&deg[k & mask], 1u);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < m;
+    const uint64_t k = valid ? keys[i] : 0ull;
+    const uint32_t u = valid ? (uint32_t)(k >> b) : 0xFFFFFFFFu;
+    const uint32_t v = valid ? (uint32_t)(k & mask) : 0xFFFFFFFFu;
+    const uint32_t uprev = __shfl_up_sync(kFull, u, 1);
+    const bool head = valid && (lane == 0 || u != uprev);
+    const unsigned hm = __ballot_sync(kFull, head), vm = __ballot_sync(kFull, valid);
+    if (head) {
+      const unsigned after = hm & ~((2u << lane) - 1u);
+      const int end = after ? __ffs(after) - 1 : 32 - __clz(vm);
+      atomicAdd(&deg[u], (uint32_t)(end - lane));
+    }
+    const unsigned peers = __match_any_sync(kFull, v);
+    if (valid && (peers & lt) == 0) atomicAdd(&deg[v], (uint32_t)__popc(peers));
   }
 }
 

@@ -95,10 +95,11 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 }
 
 // ------------------------------------------------------------- radix sort --
-constexpr int kRBlock = 256;
-constexpr int kRWarps = kRBlock / 32;
-constexpr int kRItems = 16;                   // keys per lane per tile
-constexpr int kRTile = kRBlock * kRItems;     // 4096 keys
+constexpr int kRBlock = 256;                  // histogram kernel
+constexpr int kPBlock = 512;                  // pass kernel: 16 warps x 8 keys per lane
+constexpr int kRWarps = kPBlock / 32;
+constexpr int kRItems = 8;                    // keys per lane per tile
+constexpr int kRTile = kPBlock * kRItems;     // 4096 keys
 constexpr int kRDigits = 256;
 constexpr int kRMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -136,18 +137,18 @@ __global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long lon
 
 // (2) one pass
 template <typename K>
-__global__ void __launch_bounds__(kRBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+__global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
                                                         uint32_t shift, const unsigned long long* __restrict__ base,
                                                         unsigned long long* __restrict__ status,
                                                         uint32_t* __restrict__ tile_ctr) {
   __shared__ __align__(16) K skeys[kRTile];
-  __shared__ uint32_t wcnt[kRWarps][kRDigits];
-  __shared__ uint32_t tdp[kRDigits];          // tile-local exclusive digit prefix
+  __shared__ uint16_t wcnt[kRWarps][kRDigits];   // per-warp digit counts (<= 256), then prefixes
+  __shared__ uint32_t tdp[kRDigits];             // tile-local exclusive digit prefix
   __shared__ unsigned long long goff[kRDigits];  // global position of the tile's first key with digit d
   __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < kRWarps * kRDigits; i += kRBlock) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kRWarps * kRDigits; i += kPBlock) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t t0 = tile * kRTile;
@@ -164,55 +165,75 @@ __global__ void __launch_bounds__(kRBlock) k_radix_pass(const K* __restrict__ in
     const unsigned peers = __match_any_sync(kFull, d);
     const uint32_t before = (d < 0x100u) ? wcnt[w][d] : 0u;
     __syncwarp();
-    if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = before + __popc(peers);
+    if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(before + __popc(peers));
     __syncwarp();
     rk[r] = before + __popc(peers & lt);
     dg[r] = d;
   }
   __syncthreads();
-  // thread d: per-warp exclusive prefix, tile total, tile-local digit prefix
+  // thread d < 256: per-warp exclusive prefix, tile total, look-back
   const uint32_t d = threadIdx.x;
-  uint32_t run = 0;
+  uint32_t total = 0;
+  if (d < kRDigits) {
+    uint32_t run = 0;
 #pragma unroll
-  for (int ww = 0; ww < kRWarps; ++ww) {
-    const uint32_t c = wcnt[ww][d];
-    wcnt[ww][d] = run;
-    run += c;
-  }
-  const uint32_t total = run;
-  {
-    unsigned long long* my = status + tile * kRDigits + d;
-    if (tile == 0) {
-      __stcg(my, kFlagInc | total);
-      goff[d] = base[d];
-    } else {
-      __stcg(my, kFlagAgg | total);
-      unsigned long long excl = 0;
-      uint64_t t = tile - 1;
-      for (;;) {
-        const unsigned long long sv = *((volatile unsigned long long*)(status + t * kRDigits + d));
-        const unsigned long long fl = sv & ~kValMask;
-        if (fl == 0) continue;  // predecessor has not published yet (it started before us)
-        excl += sv & kValMask;
-        if (fl == kFlagInc) break;
-        --t;
-      }
-      __stcg(my, kFlagInc | (excl + total));
-      goff[d] = base[d] + excl;
+    for (int ww = 0; ww < kRWarps; ++ww) {
+      const uint32_t c = wcnt[ww][d];
+      wcnt[ww][d] = (uint16_t)run;  // prefix <= 4096 fits u16
+      run += c;
     }
+    total = run;
   }
-  // tile-local exclusive prefix over digits
+  // publish this tile's aggregate (tile 0: its inclusive prefix) for every digit
+  __shared__ uint32_t stot[kRDigits];
+  if (d < kRDigits) {
+    stot[d] = total;
+    __stcg(status + tile * kRDigits + d, (tile == 0 ? kFlagInc : kFlagAgg) | total);
+    if (tile == 0) goff[d] = base[d];
+  }
+  __syncthreads();
+  // decoupled look-back, one thread per digit, reading a window of 8 preceding
+  // tiles per step (independent loads in flight); a tile that has not published
+  // yet stops the window and is re-read from there.
+  if (tile > 0 && d < kRDigits) {
+    constexpr int kW = 8;
+    unsigned long long excl = 0;
+    int64_t t = (int64_t)tile - 1;
+    for (;;) {
+      unsigned long long sv[kW];
+#pragma unroll
+      for (int j = 0; j < kW; ++j)
+        sv[j] = (t - j >= 0) ? *((volatile unsigned long long*)(status + (uint64_t)(t - j) * kRDigits + d)) : kFlagInc;
+      int j = 0;
+      bool done = false;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        if (done || j != q) continue;
+        const unsigned long long fl = sv[q] & ~kValMask;
+        if (fl == 0) continue;  // not published yet: stop the window here
+        excl += sv[q] & kValMask;
+        ++j;
+        if (fl == kFlagInc) done = true;
+      }
+      if (done) break;
+      t -= j;
+    }
+    __stcg(status + tile * kRDigits + d, kFlagInc | (excl + total));
+    goff[d] = base[d] + excl;
+  }
+  // tile-local exclusive prefix over digits (threads >= 256 contribute 0)
   {
-    __shared__ uint32_t sw[kRDigits / 32 + 1];
+    __shared__ uint32_t sw[kPBlock / 32 + 1];
     uint32_t tt;
-    tdp[d] = block_exclusive_scan<kRBlock>(total, sw, &tt);
+    const uint32_t ex = block_exclusive_scan<kPBlock>(total, sw, &tt);
+    if (d < kRDigits) tdp[d] = ex;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRItems; ++r)
     if (dg[r] < 0x100u) skeys[tdp[dg[r]] + wcnt[w][dg[r]] + rk[r]] = key[r];
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < tn; i += kRBlock) {
+  for (uint32_t i = threadIdx.x; i < tn; i += kPBlock) {
     const K k = skeys[i];
     const uint32_t dd = (uint32_t)(k >> shift) & 0xFFu;
     out[goff[dd] + (i - tdp[dd])] = k;
@@ -243,7 +264,7 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& 
   for (uint32_t p = 0; p < passes; ++p) {
     if (triv[p]) continue;
     EH_CUDA(cudaMemsetAsync(status.p, 0, status.bytes(), s));
-    k_radix_pass<K><<<(unsigned)tiles, kRBlock, 0, s>>>(src, dst, n, 8 * p, base.p + (size_t)p * kRDigits, status.p,
+    k_radix_pass<K><<<(unsigned)tiles, kPBlock, 0, s>>>(src, dst, n, 8 * p, base.p + (size_t)p * kRDigits, status.p,
                                                        ctr.p + p);
     EH_LAUNCH("k_radix_pass");
     K* t = src; src = dst; dst = t;
