@@ -2,58 +2,299 @@
 //
 // 4Clique(x,y,z,w) :- R(x,y),S(y,z),T(x,z),U(x,w),V(y,w),Q(z,w),
 // attribute order x, y, z, w on the pruned relation:
-//     for x:  for y in N+(x):
-//        P = N+(x) cap N+(y)                       (materialised per warp, sorted)
-//        for z in P:  K += | P cap N+(z) |        (only P after z can match)
-// Each intersection uses the same layout dispatch as the triangle kernel.
+//     for x:  for y in N+(x):  for z in N+(x) cap N+(y):
+//        K += | N+(x) cap N+(y) cap N+(z) |
+// Every 4-clique x<y<z<w (rank order) is counted once, at its lowest vertex x.
+//
+// B200 formulation (same count): for one x, index N+(x) locally
+// (x_0 < x_1 < ... < x_{d-1}) and build in shared memory the bit-matrix L of the
+// subgraph G[N+(x)]:  bit j of row i  <=>  x_j in N+(x_i)  (so j > i).  Row i is
+// the intersection N+(x) after x_i  cap  N+(x_i) -- exactly the triangle row of
+// edge (x, x_i) -- computed with the same layout dispatch:
+//   PROBE  N+(x_i) bitset: each x_j (j > i) tests its bit;
+//   STREAM N+(x_i) uint: stream its list, look each element up in a shared-memory
+//          hash of N+(x) that returns the local index j;
+//   SEARCH |A| log|B| << |B|: each x_j binary-searches N+(x_i).
+// Then the innermost loop is a bit-parallel AND:
+//     K(x) = sum over set bits (i, j) of popcount(L_i & L_j restricted to > j),
+// i.e. |P cap N+(z)| with P = N+(x) cap N+(y), y = x_i, z = x_j, counted 32 w
+// at a time.  |N+(x)| <= 128: one warp per x (rows on 8-lane groups, then 4-lane
+// groups over the <= 4 words of a row); 128 < |N+(x)| <= 1024: one CTA per x
+// (L up to 128 KB of shared memory); larger x (rare): P materialised per warp
+// in global scratch.  COUNT(*) accumulates per lane in u64 (K4 > 2^32 on C4).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
+#include "rows.cuh"
 #include "sets.cuh"
 
 namespace eh {
 
 namespace {
 
-constexpr int kK4Warps = 4;
-constexpr int kK4Block = kK4Warps * 32;
-constexpr int kK4Cap = 1024;  // N+(x) and P staged in shared memory when |N+(x)| <= kK4Cap
+constexpr int kG = 8;                 // lanes per row group (row fill)
+constexpr int kWMaxD = 128;           // warp kernel: d <= 128 -> rows of <= 4 words
+constexpr int kWW = 4;                // row stride (words) in the warp kernel
+constexpr int kWHash = 512;           // hash slots >= 4d
+constexpr int kWWarps = 8;
+constexpr int kCMaxD = 1024;          // CTA kernel: d <= 1024 -> rows of <= 32 words
+constexpr int kCHash = 4096;
+constexpr int kCWarps = 16;
+constexpr uint32_t kEmptyK = 0xFFFFFFFFu;
 
-__global__ void __launch_bounds__(kK4Block) k_k4_warp(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
-                                                      const uint32_t* __restrict__ bs,
-                                                      const uint32_t* __restrict__ work, uint64_t nwork,
-                                                      uint32_t* __restrict__ pscratch, uint32_t pstride,
-                                                      unsigned long long* __restrict__ ctr) {
-  __shared__ __align__(16) uint32_t xs_s[kK4Warps][kK4Cap];
-  __shared__ __align__(16) uint32_t ps_s[kK4Warps][kK4Cap];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+enum K4Kind : uint8_t { kKSkip = 0, kKProbe = 1, kKStream = 2, kKSearch = 3 };
+
+// N+(x) -> local index, open addressing (load <= 1/4)
+struct LocalHash {
+  const uint32_t* keys;
+  const uint16_t* idx;
+  uint32_t shift, mask, amin, amax;
+  __device__ __forceinline__ int lookup(uint32_t e) const {
+    if (e < amin || e > amax) return -1;
+    uint32_t s = (e * 2654435761u) >> shift;
+    for (;;) {
+      const uint32_t v = keys[s];
+      if (v == e) return idx[s];
+      if (v == kEmptyK) return -1;
+      s = (s + 1) & mask;
+    }
+  }
+};
+
+template <bool kCta>
+__device__ __forceinline__ LocalHash build_local_hash(uint32_t* keys, uint16_t* idx, const uint32_t* xs, uint32_t d,
+                                                      int tid, int nt) {
+  uint32_t hbits = 5;
+  while ((1u << hbits) < 4 * d) ++hbits;
+  LocalHash H{keys, idx, 32 - hbits, (1u << hbits) - 1u, xs[0], xs[d - 1]};
+  for (uint32_t k = tid; k < (1u << hbits); k += nt) keys[k] = kEmptyK;
+  if (kCta) __syncthreads(); else __syncwarp();
+  for (uint32_t k = tid; k < d; k += nt) {
+    const uint32_t e = xs[k];
+    uint32_t h = (e * 2654435761u) >> H.shift;
+    while (atomicCAS(&keys[h], kEmptyK, e) != kEmptyK) h = (h + 1) & H.mask;
+    idx[h] = (uint16_t)k;
+  }
+  return H;
+}
+
+__device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a) {
+  if (a == 0 || y.len == 0) return kKSkip;
+  if (y.c1 > y.c0) return kKProbe;
+  const uint32_t lg = 32 - __clz(y.len);
+  if ((uint64_t)a * lg * 4 < y.len) return kKSearch;
+  return kKStream;
+}
+
+// Fill row i of L (stride W words) with the 8-lane group's lane gl.
+__device__ __forceinline__ void fill_row(uint8_t kd, const uint32_t* __restrict__ col, const uint32_t* __restrict__ bs,
+                                         const YInfo& y, const uint32_t* xs, uint32_t d, uint32_t i, const LocalHash& H,
+                                         uint32_t* Lrow, uint32_t gl) {
+  if (kd == kKProbe) {
+    for (uint32_t j = i + 1 + gl; j < d; j += kG)
+      if (probe_bits(bs, y, xs[j])) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
+  } else if (kd == kKStream) {
+    const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
+    const uint32_t nfull = y.len >> 2;
+    for (uint32_t k = gl; k < nfull; k += kG) {
+      const uint4 v = __ldg(yl + k);
+      const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = H.lookup(e[q]);
+        if (j >= 0) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
+      }
+    }
+    if (gl < (y.len & 3)) {
+      const int j = H.lookup(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + gl));
+      if (j >= 0) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
+    }
+  } else if (kd == kKSearch) {
+    for (uint32_t j = i + 1 + gl; j < d; j += kG)
+      if (gmem_search(col + (uint64_t)y.list * 4, y.len, xs[j])) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
+  }
+}
+
+// ------------------------------------------------------------ warp kernel --
+struct __align__(16) K4WarpSmem {
+  uint32_t xs[kWMaxD];
+  uint32_t hkeys[kWHash];
+  uint32_t L[kWMaxD * kWW];
+  YInfo yi[kWMaxD];
+  uint16_t hidx[kWHash];
+  uint8_t kind[kWMaxD];
+  uint8_t ord[kWMaxD];
+};
+
+__global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restrict__ desc,
+                                                          const uint32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ bs,
+                                                          const uint32_t* __restrict__ work, uint64_t nwork,
+                                                          unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) uint32_t dsm_k4w[];
+  K4WarpSmem& sm = reinterpret_cast<K4WarpSmem*>(dsm_k4w)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const uint64_t gw = (uint64_t)blockIdx.x * kK4Warps + w;
   unsigned long long cnt = 0;
   for (;;) {
     unsigned long long wi = 0;
     if (lane == 0) wi = atomicAdd(&ctr[1], 1ull);
     wi = __shfl_sync(kFull, wi, 0);
     if (wi >= nwork) break;
-    const uint32_t x = work[wi];
-    const uint4 dx = desc[x];
-    const uint32_t d = dx.y;
+    const uint32_t x = __ldg(work + wi);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;  // 2 <= d <= kWMaxD
     if (d < 3) continue;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
-    const uint32_t* xs = xg;
-    uint32_t* P = pscratch ? pscratch + gw * pstride : nullptr;
-    if (d <= kK4Cap) {
-      const uint4* src4 = reinterpret_cast<const uint4*>(xg);
-      uint4* dst4 = reinterpret_cast<uint4*>(xs_s[w]);
-      for (uint32_t k = lane; k < (d + 3) / 4; k += 32) dst4[k] = __ldg(src4 + k);
-      __syncwarp();
-      xs = xs_s[w];
-      P = ps_s[w];
+    for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
+      reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
+    for (uint32_t k = lane; k < d * kWW; k += 32) sm.L[k] = 0u;
+    __syncwarp();
+    const LocalHash H = build_local_hash<false>(sm.hkeys, sm.hidx, sm.xs, d, lane, 32);
+    const uint32_t nrows = d - 1;
+    for (uint32_t i = lane; i < nrows; i += 32) {
+      const YInfo y = yinfo(desc, sm.xs[i]);
+      sm.yi[i] = y;
+      sm.kind[i] = k4_kind(y, nrows - i);
     }
+    __syncwarp();
+    uint32_t nr = 0;
+#pragma unroll
+    for (int kdi = 0; kdi < 3; ++kdi) {
+      const uint8_t want = (uint8_t)(kKProbe + kdi);
+      for (uint32_t i0 = 0; i0 < nrows; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool sel = i < nrows && sm.kind[i] == want;
+        const unsigned m = __ballot_sync(kFull, sel);
+        if (sel) sm.ord[nr + __popc(m & lt)] = (uint8_t)i;
+        nr += __popc(m);
+      }
+    }
+    __syncwarp();
+    for (uint32_t r = lane / kG; r < nr; r += 32 / kG) {
+      const uint32_t i = sm.ord[r];
+      fill_row(sm.kind[i], col, bs, sm.yi[i], sm.xs, d, i, H, sm.L + i * kWW, lane % kG);
+    }
+    __syncwarp();
+    // bit-parallel innermost loop: 4-lane groups, lane q holds word q of row i
+    const uint32_t W = (d + 31) >> 5, q = lane & 3;
+    for (uint32_t i0 = 0; i0 < d; i0 += 8) {
+      const uint32_t i = i0 + (lane >> 2);
+      const uint32_t li = (i < d && q < W) ? sm.L[i * kWW + q] : 0u;
+      for (uint32_t kk = 0; kk < W; ++kk) {
+        uint32_t wb = __shfl_sync(kFull, li, (lane & ~3) + kk);
+        while (wb) {
+          const uint32_t b = __ffs(wb) - 1;
+          wb &= wb - 1;
+          const uint32_t j = kk * 32 + b;
+          if (q >= kk && q < W) {
+            const uint32_t m = (q == kk) ? ~((2u << b) - 1u) : 0xFFFFFFFFu;
+            cnt += __popc(li & sm.L[j * kWW + q] & m);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
+}
+
+// ------------------------------------------------------------- CTA kernel --
+__global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict__ desc,
+                                                          const uint32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ bs,
+                                                          const uint32_t* __restrict__ work, uint64_t nwork,
+                                                          unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) uint32_t dsm_k4c[];
+  uint32_t* xs = dsm_k4c;                                   // kCMaxD
+  uint32_t* hkeys = xs + kCMaxD;                            // kCHash
+  uint16_t* hidx = reinterpret_cast<uint16_t*>(hkeys + kCHash);  // kCHash u16
+  uint32_t* L = hkeys + kCHash + kCHash / 2;                // d * W words
+  __shared__ unsigned long long s_wi;
+  constexpr uint32_t kGroups = kCWarps * 32 / kG;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t gid = threadIdx.x / kG, gl = threadIdx.x % kG;
+  unsigned long long cnt = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
+    __syncthreads();
+    const unsigned long long wi = s_wi;
+    if (wi >= nwork) break;
+    const uint32_t x = __ldg(work + wi);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;
+    if (d > (uint32_t)kCMaxD || d < 3) {  // other classes handle these
+      __syncthreads();
+      continue;
+    }
+    const uint32_t W = (d + 31) >> 5;
+    const uint32_t* xg = col + (uint64_t)dx.x * 4;
+    for (uint32_t k = threadIdx.x; k < (d + 3) / 4; k += blockDim.x)
+      reinterpret_cast<uint4*>(xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
+    for (uint32_t k = threadIdx.x; k < d * W; k += blockDim.x) L[k] = 0u;
+    __syncthreads();
+    const LocalHash H = build_local_hash<true>(hkeys, hidx, xs, d, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const uint32_t nrows = d - 1;
+    uint32_t i = gid;
+    YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
+    while (i < nrows) {
+      const uint32_t inext = i + kGroups;
+      const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
+      fill_row(k4_kind(y, nrows - i), col, bs, y, xs, d, i, H, L + i * W, gl);
+      i = inext;
+      y = ynext;
+    }
+    __syncthreads();
+    // bit-parallel innermost loop: one warp per row, lane k holds word k
+    for (uint32_t r = w; r < d; r += kCWarps) {
+      const uint32_t li = ((uint32_t)lane < W) ? L[r * W + lane] : 0u;
+      for (uint32_t kk = 0; kk < W; ++kk) {
+        uint32_t wb = __shfl_sync(kFull, li, kk);
+        while (wb) {
+          const uint32_t b = __ffs(wb) - 1;
+          wb &= wb - 1;
+          const uint32_t j = kk * 32 + b;
+          if ((uint32_t)lane >= kk && (uint32_t)lane < W) {
+            const uint32_t m = ((uint32_t)lane == kk) ? ~((2u << b) - 1u) : 0xFFFFFFFFu;
+            cnt += __popc(li & L[j * W + lane] & m);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
+}
+
+constexpr size_t kCtaSmemK4 = (size_t)(kCMaxD + kCHash + kCHash / 2 + kCMaxD * (kCMaxD / 32)) * 4;
+
+// ------------------------------------------- fallback: |N+(x)| > kCMaxD --
+// P = N+(x) after y cap N+(y) materialised per warp (global scratch), then
+// for z in P: |P after z cap N+(z)| by membership probes.
+__global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
+                                                 const uint32_t* __restrict__ bs, const uint32_t* __restrict__ work,
+                                                 uint64_t nwork, uint32_t* __restrict__ pscratch, uint32_t pstride,
+                                                 unsigned long long* __restrict__ ctr) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t* P = pscratch + gw * pstride;
+  unsigned long long cnt = 0;
+  for (;;) {
+    unsigned long long wi = 0;
+    if (lane == 0) wi = atomicAdd(&ctr[3], 1ull);
+    wi = __shfl_sync(kFull, wi, 0);
+    if (wi >= nwork) break;
+    const uint32_t x = __ldg(work + wi);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;
+    if (d <= (uint32_t)kCMaxD) continue;
+    const uint32_t* xs = col + (uint64_t)dx.x * 4;
     for (uint32_t i = 0; i + 2 < d; ++i) {
-      const uint32_t y = xs[i];
-      const SetRef sy = set_of(desc, col, bs, y);
+      const SetRef sy = set_of(desc, col, bs, xs[i]);
       if (sy.len < 2) continue;
-      // P = (N+(x) after y) cap N+(y), kept in increasing order via ballot compaction
       uint32_t np = 0;
       for (uint32_t j0 = i + 1; j0 < d; j0 += 32) {
         const uint32_t j = j0 + lane;
@@ -64,7 +305,6 @@ __global__ void __launch_bounds__(kK4Block) k_k4_warp(const uint4* __restrict__ 
         np += __popc(mask);
       }
       __syncwarp();
-      // for z in P: K += |P after z cap N+(z)|
       for (uint32_t t = 0; t + 1 < np; ++t) {
         const SetRef sz = set_of(desc, col, bs, P[t]);
         if (sz.len == 0) continue;
@@ -81,23 +321,33 @@ __global__ void __launch_bounds__(kK4Block) k_k4_warp(const uint4* __restrict__ 
 
 uint64_t count_4cliques(eh_graph* g) {
   cudaStream_t s = g->stream;
-  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 2 * sizeof(unsigned long long), s));
-  const uint64_t nwork = g->n_work[0] + g->n_work[1] + g->n_work[2];
-  if (nwork) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((nwork + kK4Warps - 1) / kK4Warps, (uint64_t)kSMs * 4);
-    DBuf<uint32_t> scratch;
-    uint32_t stride = 0;
-    if (g->max_dplus > (uint64_t)kK4Cap) {
-      stride = (uint32_t)g->max_dplus;
-      scratch = DBuf<uint32_t>(g->alloc, (size_t)grid * kK4Warps * stride);
+  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
+  const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
+  const uint64_t nlarge = g->n_work[2];
+  const uint32_t* wl = g->work + nsmall;
+  if (nlarge) {
+    EH_CUDA(cudaFuncSetAttribute(k_k4_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemK4));
+    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
+    k_k4_cta<<<grid, kCWarps * 32, kCtaSmemK4, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter);
+    EH_LAUNCH("k_k4_cta");
+    if (g->max_dplus > (uint64_t)kCMaxD) {
+      const unsigned gb = (unsigned)kSMs * 4;
+      const uint32_t stride = (uint32_t)g->max_dplus;
+      DBuf<uint32_t> scratch(g->alloc, (size_t)gb * 4 * stride);
+      k_k4_big<<<gb, 128, 0, s>>>(g->desc, g->col, g->bs, wl, nlarge, scratch.p, stride, g->d_counter);
+      EH_LAUNCH("k_k4_big");
     }
-    k_k4_warp<<<grid, kK4Block, 0, s>>>(g->desc, g->col, g->bs, g->work, nwork, scratch.p, stride, g->d_counter);
-    EH_LAUNCH("k_k4_warp");
-    EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    EH_CUDA(cudaStreamSynchronize(s));
-    return g->h_counter[0];
   }
-  return 0;
+  if (nsmall) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
+    const size_t smem = sizeof(K4WarpSmem) * kWWarps;
+    EH_CUDA(cudaFuncSetAttribute(k_k4_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_k4_warp<<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    EH_LAUNCH("k_k4_warp");
+  }
+  EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  return g->h_counter[0];
 }
 
 }  // namespace eh

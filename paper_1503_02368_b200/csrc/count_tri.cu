@@ -31,6 +31,7 @@
 // (PAPER.md:243).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
+#include "rows.cuh"
 #include "sets.cuh"
 
 namespace eh {
@@ -50,35 +51,6 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 enum RowKind : uint8_t { kSkip = 0, kProbe = 1, kAnd = 2, kStream = 3, kSearchGlobal = 4 };
 enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2 };
-
-struct YInfo {
-  uint32_t list;  // col offset of N+(y) in 16-B units
-  uint32_t len;   // |N+(y)|
-  uint32_t pool;  // bitset pool offset of chunk c0 in 16-B chunks (if bitset)
-  uint32_t c0;    // first chunk
-  uint32_t c1;    // one past last chunk (c1 == c0: no bitset)
-};
-
-__device__ __forceinline__ YInfo yinfo(const uint4* __restrict__ desc, uint32_t y) {
-  const uint4 d = __ldg(desc + y);
-  const uint32_t z1 = __ldg(&desc[y + 1].z);
-  return YInfo{d.x, d.y, d.z, d.w, d.w + (z1 - d.z)};
-}
-
-__device__ __forceinline__ uint32_t probe_bits(const uint32_t* __restrict__ bs, const YInfo& y, uint32_t e) {
-  const uint32_t c = e >> 7;
-  if (c < y.c0 || c >= y.c1) return 0u;
-  return (__ldg(bs + (uint64_t)y.pool * 4 + ((e >> 5) - 4u * y.c0)) >> (e & 31)) & 1u;
-}
-
-__device__ __forceinline__ uint32_t gmem_search(const uint32_t* __restrict__ a, uint32_t n, uint32_t e) {
-  uint32_t lo = 0, len = n;
-  while (len > 0) {
-    const uint32_t h = len >> 1;
-    if (__ldg(a + lo + h) < e) { lo += h + 1; len -= h + 1; } else { len = h; }
-  }
-  return (lo < n && __ldg(a + lo) == e) ? 1u : 0u;
-}
 
 // ---------------------------------------------- x's membership structure --
 // N+(x) in shared memory as (a) an exact bitmap over [lo, lo + nbits), (b) an
