@@ -41,6 +41,16 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402  (input generator; no method arithmetic)
 
 
+METRIC = "triangles counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)"
+
+
+def _workload(cfg) -> str:
+    if cfg.kind == "er":
+        return f"{cfg.name}: ER G(n={cfg.n}, p={cfg.p}), seed {cfg.seed}; triangle count"
+    return (f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, (a,b,c)=(.57,.19,.19), "
+            f"seed {cfg.seed}; triangle count")
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -64,7 +74,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -120,6 +130,16 @@ def _max_over_ranks(dist, val: float, device) -> float:
     return float(t.item())
 
 
+def _traffic():
+    """DRAM bytes (read + write) per launch of the count kernels, from the
+    committed `ncu --set full` capture (profiles/traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("tri_C3_bytes_per_launch")
+    return None
+
+
 def _flush_l2(buf):
     if os.environ.get("BENCH_NOFLUSH") != "1":
         buf.add_(1)  # 512 MiB write: > 2x the 126 MB L2
@@ -170,12 +190,11 @@ def run_reference(args, cfg, src, dst, n_in):
     sample = (f"oracle ingest of the full {cfg.name} input timed once ({t_ing:.2f} s); each step = one 1/{S} "
               f"slice of the outer x loop of the triangle nest + 1/{S} of the ingest time; value = n_in / "
               f"(64 x mean step)")
-    line = {"impl": "reference", "metric": "triangles counted: input edges/sec", "value": value,
+    line = {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "input edges/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, seed {cfg.seed}",
-                       "n_input": n_in},
+            "config": {"workload": _workload(cfg), "n_input": n_in},
             "cpu_baseline": {"value": value, "unit": "input edges/s", "cores": threads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "input edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -201,8 +220,9 @@ def run_gpu(args, cfg, src, dst, n_in):
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MiB
     torch.cuda.synchronize()
 
-    def one_step(host: bool):
-        """Returns (t_step_ms, t_count_ms, count, stats)."""
+    def one_step(host: bool, want_stats: bool = False):
+        """Returns (t_step_ms, t_count_ms, count, stats or None).  Statistics are
+        computed on demand by the library, outside the step's events."""
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         with torch.cuda.stream(stream):
             ev[0].record(stream)
@@ -213,7 +233,8 @@ def run_gpu(args, cfg, src, dst, n_in):
             ev[1].record(stream)
             c = g.count_triangles()
             ev[2].record(stream)
-            st = g.stats()
+            stream.synchronize()
+            st = g.stats() if want_stats else None
             g.close()
         stream.synchronize()
         return ev[0].elapsed_time(ev[2]), ev[1].elapsed_time(ev[2]), c, st
@@ -230,15 +251,15 @@ def run_gpu(args, cfg, src, dst, n_in):
     clocks.start()
     l0 = eh.launch_count()
     step_ms, count_ms, counts = [], [], set()
-    st = None
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             _flush_l2(flush)  # outside the per-step events
-        t, tc, c, st = one_step(False)
+        t, tc, c, _ = one_step(False)
         step_ms.append(t)
         count_ms.append(tc)
         counts.add(c)
     launches = (eh.launch_count() - l0) / max(1, args.steps)
+    st = one_step(False, want_stats=True)[3]  # untimed: B_tri and sizes for the report
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -264,12 +285,11 @@ def run_gpu(args, cfg, src, dst, n_in):
     value = ws * n_in / (mean_step_max / 1e3)
     achieved = st.alg_bytes_tri / (mean_count / 1e3) / 1e9
     line = {
-        "metric": "triangles counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)",
+        "metric": METRIC,
         "value": value, "unit": "input edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean_step_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, "
-                               f"(a,b,c)=(.57,.19,.19), seed {cfg.seed}; triangle count",
+        "config": {"workload": _workload(cfg),
                    "n_input": n_in, "m_undirected": st.m_undirected, "n_active": st.n_active,
                    "parallelism": "replicas only" if ws > 1 else "1 GPU",
                    "l2": "512 MiB flush write between timed steps (outside the per-step events); inputs 537 MB > L2",
@@ -279,7 +299,7 @@ def run_gpu(args, cfg, src, dst, n_in):
         "count_edges_per_s": n_in / (mean_count / 1e3),
         "triangles_per_s": T / (mean_count / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "kernel": "k_tri_*  (eh_count_triangles)",
+                     "traffic": _traffic(), "peak_kind": peak_kind, "kernel": "k_tri_*  (eh_count_triangles)",
                      "alg_bytes_per_launch": st.alg_bytes_tri},
         "e2e": {"value": ws * n_in / (mean_e2e_max / 1e3), "unit": "input edges/s",
                 "h2d_bytes_per_step": 8 * n_in, "d2h_bytes_per_step": 8},

@@ -171,6 +171,12 @@ int eh_graph_stats(const eh_graph* g, eh_stats* out) {
     set_status(EH_EINVAL, "eh_graph_stats: NULL argument");
     return EH_EINVAL;
   }
+  const int rc = guarded<int>(EH_ECUDA, [&]() -> int {
+    DeviceGuard guard(g->device);
+    eh::compute_stats(const_cast<eh_graph*>(g));  // cached, logically const
+    return EH_OK;
+  });
+  if (rc != EH_OK) return t_status;
   out->n_input = g->n_input;
   out->m_undirected = g->m;
   out->n_active = g->n_act;

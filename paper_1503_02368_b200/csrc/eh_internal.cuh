@@ -205,6 +205,8 @@ struct eh_graph {
   uint32_t* col = nullptr;      // padded per list to 4 elements with kNone
   uint32_t* bs = nullptr;       // bitset pool (128-bit aligned chunks at absolute id/128)
   uint32_t* orig_id = nullptr;  // original id of each rank
+  uint32_t* bytes32 = nullptr;  // bytes(N+(v)) at tau = 32 (B_tri accounting)
+  bool stats_ready = false;
   // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
   uint32_t* work = nullptr;
   uint64_t n_work[3] = {0, 0, 0};
@@ -227,6 +229,7 @@ namespace eh {
 void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, PhaseTimer* t = nullptr);
 // trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
 void build_layouts(eh_graph* g);
+void compute_stats(eh_graph* g);  // lazy: B_tri, wedge work, #bitset sets
 void build_worklists(eh_graph* g);
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);

@@ -118,9 +118,10 @@ void build_layouts(eh_graph* g) {
     g->bs = (uint32_t*)g->own(16);
     return;
   }
-  DBuf<uint32_t> nch(al, n), c0(al, n), bytes(al, n);
+  DBuf<uint32_t> nch(al, n), c0(al, n);
+  g->bytes32 = (uint32_t*)g->own(n * 4);  // kept for the on-demand statistics (compute_stats)
   k_layout<<<grid_for(n, TB * 4), TB, 0, s>>>(g->desc, g->col, n, g->tau, g->min_bitset_card,
-                                              (g->flags & EH_ALL_UINT) != 0, nch.p, c0.p, bytes.p);
+                                              (g->flags & EH_ALL_UINT) != 0, nch.p, c0.p, g->bytes32);
   EH_LAUNCH("k_layout");
   DBuf<uint64_t> off(al, n), tot(al, 1);
   scan_exclusive_u32(nch.p, off.p, n, tot.p, al, s);
@@ -135,16 +136,30 @@ void build_layouts(eh_graph* g) {
     k_fill_bitsets<<<grid_for(n * 32, TB), TB, 0, s>>>(g->desc, g->col, n, g->bs);
     EH_LAUNCH("k_fill_bitsets");
   }
-  DBuf<unsigned long long> st(al, 4);
-  EH_CUDA(cudaMemsetAsync(st.p, 0, 4 * sizeof(unsigned long long), s));
-  k_stats<<<grid_for(n * 32, TB), TB, 0, s>>>(g->desc, g->col, n, bytes.p, st.p);
-  EH_LAUNCH("k_stats");
-  unsigned long long h[4];
-  EH_CUDA(cudaMemcpyAsync(h, st.p, sizeof h, cudaMemcpyDeviceToHost, s));
-  EH_CUDA(cudaStreamSynchronize(s));
-  g->alg_bytes_tri = 8ull * (n + 1) + h[1] + h[0];
-  g->wedge_work = h[2];
-  g->n_bitsets = h[3];
+}
+
+// Statistics that are not needed by the counts (B_tri, wedge work, number of
+// bitset sets) are computed on the first eh_graph_stats call, off the load path.
+void compute_stats(eh_graph* g) {
+  if (g->stats_ready) return;
+  const uint64_t n = g->n_act;
+  if (n) {
+    cudaStream_t s = g->stream;
+    const unsigned TB = 256;
+    DBuf<unsigned long long> st(g->alloc, 4);
+    EH_CUDA(cudaMemsetAsync(st.p, 0, 4 * sizeof(unsigned long long), s));
+    k_stats<<<grid_for(n * 32, TB), TB, 0, s>>>(g->desc, g->col, n, g->bytes32, st.p);
+    EH_LAUNCH("k_stats");
+    unsigned long long h[4];
+    EH_CUDA(cudaMemcpyAsync(h, st.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    EH_CUDA(cudaStreamSynchronize(s));
+    g->alg_bytes_tri = 8ull * (n + 1) + h[1] + h[0];
+    g->wedge_work = h[2];
+    g->n_bitsets = h[3];
+  } else {
+    g->alg_bytes_tri = 8;
+  }
+  g->stats_ready = true;
 }
 
 void build_worklists(eh_graph* g) {

@@ -234,3 +234,45 @@ def test_intersect_device_and_errors():
     assert ei.value.status == eh.EH_EUNSORTED
     with pytest.raises(eh.EHError):
         eh.intersect(np.array([2, 2], np.uint32), np.array([1], np.uint32))
+
+
+# ------------------------------------------------------------ error paths (T8) --
+def test_allocator_hook_failure_is_enomem():
+    """An allocator hook that returns NULL makes eh_load_edges fail cleanly with EH_ENOMEM."""
+    import ctypes
+    from paper_1503_02368_b200 import eh as ehmod
+    L = ehmod.lib()
+    alloc = ehmod._ALLOC_FN(lambda size, stream, ctx: None)
+    free = ehmod._FREE_FN(lambda p, stream, ctx: None)
+    src, dst = synth.rmat(10, 8, 1)
+    cfg = ehmod.EHConfig()
+    cfg.dev_alloc = alloc
+    cfg.dev_free = free
+    h = L.eh_load_edges_ex(src.ctypes.data, dst.ctypes.data, src.size, ctypes.byref(cfg))
+    assert h is None and L.eh_last_status() == eh.EH_ENOMEM
+    # the library stays usable afterwards
+    assert _gpu_counts(src, dst)[0] == oracle.count_triangles(src, dst)
+
+
+def test_invalid_device_and_graph_handles():
+    import ctypes
+    from paper_1503_02368_b200 import eh as ehmod
+    L = ehmod.lib()
+    cfg = ehmod.EHConfig()
+    cfg.flags = eh.EH_SET_DEVICE
+    cfg.device = 4096
+    src, dst = synth.rmat(8, 8, 1)
+    assert L.eh_load_edges_ex(src.ctypes.data, dst.ctypes.data, src.size, ctypes.byref(cfg)) is None
+    assert L.eh_last_status() == eh.EH_EINVAL
+    with pytest.raises(eh.EHError):
+        eh.Graph(src, dst[:-1])
+
+
+def test_repeated_counts_and_many_handles():
+    """A handle is immutable after load: repeated counts agree; handles are independent."""
+    graphs = [eh.Graph(*synth.rmat(11, 8, s)) for s in range(6)]
+    first = [g.count_triangles() for g in graphs]
+    again = [g.count_triangles() for g in reversed(graphs)][::-1]
+    assert first == again
+    for g in graphs:
+        g.close()

@@ -1,0 +1,54 @@
+"""Write tests/golden/configs_oracle.json: the CPU ORACLE's counts for the five
+BASELINE.json configs, with the input checksum (synth.checksum) they belong to.
+
+Calls only synth/ (inputs) and oracle/ (counts) -- never the CUDA path -- so the
+stored values are oracle values (task rule: "a stored value is ... written by a
+committed script that calls only oracle/").  Usage:
+    python tools/write_oracle_goldens.py C1 C2 C3 C4 C5
+Existing entries for other configs are kept.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "configs_oracle.json")
+
+
+def main(names):
+    data = json.load(open(OUT)) if os.path.exists(OUT) else {
+        "citation": "BASELINE.json configs (SURVEY.md §8 C1..C5); values computed by oracle/eh_oracle.c "
+                    "via tools/write_oracle_goldens.py on synthetic inputs from synth/ (DESIGN.md §4)",
+        "configs": {}}
+    for name in names:
+        cfg = synth.CONFIGS[name]
+        t0 = time.time()
+        src, dst = cfg.generate()
+        ck = synth.checksum(src, dst)
+        t1 = time.time()
+        g = oracle.Graph(src, dst)
+        del src, dst
+        t2 = time.time()
+        entry = {"n_input": g.n_input, "m_undirected": g.m, "n_active": g.n_vertices,
+                 "max_out_degree": g.max_out_degree, "checksum": str(ck)}
+        entry["triangles"] = g.count_triangles()
+        t3 = time.time()
+        if cfg.query == "4cliques":
+            entry["four_cliques"] = g.count_4cliques()
+        t4 = time.time()
+        entry["oracle_seconds"] = {"generate": round(t1 - t0, 1), "ingest": round(t2 - t1, 1),
+                                   "triangles": round(t3 - t2, 1), "four_cliques": round(t4 - t3, 1),
+                                   "threads": oracle.default_threads()}
+        g.close()
+        data["configs"][name] = entry
+        json.dump(data, open(OUT, "w"), indent=1)
+        print(name, entry, flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["C1", "C2", "C3", "C4"])
