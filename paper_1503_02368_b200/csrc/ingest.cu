@@ -16,6 +16,7 @@
 #include "primitives.cuh"
 
 #include <algorithm>
+#include <cstring>
 
 namespace eh {
 
@@ -54,6 +55,41 @@ __global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __rest
     keys[i] = (u == v) ? sentinel : (((uint64_t)min(u, v) << b) | (uint64_t)max(u, v));
   }
 }
+
+// a1-a3 fused: canonical key (min << b) | max of every non-loop pair inserted
+// into an open-addressing hash set (linear probing; read before CAS, so the
+// duplicates that are already present cost no atomic).  Empty slot = all ones,
+// which no canonical key of a non-loop pair can equal.
+__global__ void k_hash_insert(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                              uint32_t b, unsigned long long* __restrict__ tab, uint32_t tbits) {
+  const unsigned long long kEmpty = ~0ull;
+  const uint64_t mask = (1ull << tbits) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = src[i], v = dst[i];
+    if (u == v) continue;
+    const unsigned long long key = ((uint64_t)min(u, v) << b) | (uint64_t)max(u, v);
+    uint64_t h = (key * 0x9E3779B97F4A7C15ull) >> (64 - tbits);
+    for (;;) {
+      unsigned long long cur = __ldcg(tab + h);
+      if (cur == key) break;
+      if (cur == kEmpty) {
+        cur = atomicCAS(tab + h, kEmpty, key);
+        if (cur == kEmpty || cur == key) break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+struct OccupiedPred {
+  const unsigned long long* t;
+  __device__ bool operator()(uint64_t i) const { return t[i] != ~0ull; }
+};
+struct CopySlotEmit {
+  const unsigned long long* t;
+  uint64_t* out;
+  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = t[i]; }
+};
 
 struct UniqueKeyPred {  // a3: first of a run of equal keys, sentinel excluded
   const uint64_t* k;
@@ -216,20 +252,42 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   const uint32_t b = std::max<uint32_t>(1, bitlen(n_ids - 1));
   const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
 
-  // ---- a1/a2: canonical keys + radix sort over the 2b significant bits
-  DBuf<uint64_t> keys(al, n), alt(al, n);
-  k_canon<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, keys.p);
-  EH_LAUNCH("k_canon");
+  // ---- a1-a3: canonical keys, deduplicated.  Default: radix sort over the 2b
+  // significant bits, then unique adjacent keys.  EH_DEDUP=hash selects a fused
+  // canonicalise + GPU hash-set insert (load <= ~0.6) and a compaction of the
+  // occupied slots (the downstream steps only need the DISTINCT edges); it was
+  // measured slower on C3 (random DRAM sectors, and the unsorted output slows
+  // the CSR scatter), so it is kept as an ablation.
+  uint64_t m = 0;
+  DBuf<uint64_t> keys, alt;
+  uint64_t* ukeys = nullptr;
+  const char* dd_env = getenv("EH_DEDUP");
+  if (!(dd_env && strcmp(dd_env, "hash") == 0)) {
+    keys = DBuf<uint64_t>(al, n);
+    alt = DBuf<uint64_t>(al, n);
+    k_canon<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, keys.p);
+    EH_LAUNCH("k_canon");
+    mark("canon");
+    uint64_t* sk = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);
+    mark("sort1");
+    uint64_t* other = (sk == keys.p) ? alt.p : keys.p;
+    m = select_if(n, UniqueKeyPred{sk, sentinel}, CopyKeyEmit{sk, other}, al, s);
+    ukeys = other;
+  } else {
+    uint32_t tbits = 10;
+    while ((1ull << tbits) < n + n / 2 + n / 10) ++tbits;
+    DBuf<unsigned long long> tab(al, 1ull << tbits);
+    EH_CUDA(cudaMemsetAsync(tab.p, 0xFF, tab.bytes(), s));
+    k_hash_insert<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, tab.p, tbits);
+    EH_LAUNCH("k_hash_insert");
+    mark("hash_insert");
+    // m <= n: compact into an n-sized buffer
+    keys = DBuf<uint64_t>(al, std::max<uint64_t>(1, n));
+    m = select_if(1ull << tbits, OccupiedPred{tab.p}, CopySlotEmit{tab.p, keys.p}, al, s);
+    ukeys = keys.p;
+  }
   msrc.reset();
   mdst.reset();
-  mark("canon");
-  uint64_t* sk = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);
-  mark("sort1");
-  uint64_t* other = (sk == keys.p) ? alt.p : keys.p;
-
-  // ---- a3: dedup (unique adjacent keys, sentinel dropped) -> m distinct undirected edges
-  const uint64_t m = select_if(n, UniqueKeyPred{sk, sentinel}, CopyKeyEmit{sk, other}, al, s);
-  uint64_t* ukeys = other;
   g->m = m;
   mark("dedup");
 

@@ -96,10 +96,7 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 
 // ------------------------------------------------------------- radix sort --
 constexpr int kRBlock = 256;                  // histogram kernel
-constexpr int kPBlock = 512;                  // pass kernel: 16 warps x 8 keys per lane
-constexpr int kRWarps = kPBlock / 32;
-constexpr int kRItems = 8;                    // keys per lane per tile
-constexpr int kRTile = kPBlock * kRItems;     // 4096 keys
+constexpr int kRadixDefaultCfg = 0;           // pass kernel tile: 512 threads x 8 keys (see radix_impl)
 constexpr int kRDigits = 256;
 constexpr int kRMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -136,13 +133,16 @@ __global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long lon
 }
 
 // (2) one pass
-template <typename K>
+template <typename K, int kPBlock, int kRItems>
 __global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
                                                         uint32_t shift, const unsigned long long* __restrict__ base,
                                                         unsigned long long* __restrict__ status,
                                                         uint32_t* __restrict__ tile_ctr) {
-  __shared__ __align__(16) K skeys[kRTile];
-  __shared__ uint16_t wcnt[kRWarps][kRDigits];   // per-warp digit counts (<= 256), then prefixes
+  constexpr int kRWarps = kPBlock / 32;
+  constexpr int kRTile = kPBlock * kRItems;
+  extern __shared__ __align__(16) unsigned char dsm_radix[];
+  K* skeys = reinterpret_cast<K*>(dsm_radix);    // kRTile keys (dynamic shared memory)
+  __shared__ uint16_t wcnt[kRWarps][kRDigits];   // per-warp digit counts (<= 32 * items), then prefixes
   __shared__ uint32_t tdp[kRDigits];             // tile-local exclusive digit prefix
   __shared__ unsigned long long goff[kRDigits];  // global position of the tile's first key with digit d
   __shared__ uint32_t s_tile;
@@ -256,16 +256,39 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& 
   uint32_t triv[kRMaxPasses];
   EH_CUDA(cudaMemcpyAsync(triv, trivial.p, sizeof triv, cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
-  const uint64_t tiles = (n + kRTile - 1) / kRTile;
+  // tile shape (threads x keys per thread); EH_RADIX_CFG selects one for tuning
+  static const int cfg_env = [] { const char* e = getenv("EH_RADIX_CFG"); return e ? atoi(e) : -1; }();
+  const int cfg = (cfg_env >= 0 && cfg_env <= 3) ? cfg_env : kRadixDefaultCfg;
+  static const int kThreads[4] = {512, 256, 256, 1024}, kItems[4] = {8, 8, 16, 8};
+  const uint64_t tile = (uint64_t)kThreads[cfg] * kItems[cfg];
+  const uint64_t tiles = (n + tile - 1) / tile;
   if (tiles >= (1ull << 31)) fail(EH_EINVAL, "radix sort: too many keys");
   DBuf<unsigned long long> status(al, (size_t)tiles * kRDigits);
+  const size_t smem = tile * sizeof(K);
   K* src = keys;
   K* dst = alt;
   for (uint32_t p = 0; p < passes; ++p) {
     if (triv[p]) continue;
     EH_CUDA(cudaMemsetAsync(status.p, 0, status.bytes(), s));
-    k_radix_pass<K><<<(unsigned)tiles, kPBlock, 0, s>>>(src, dst, n, 8 * p, base.p + (size_t)p * kRDigits, status.p,
-                                                       ctr.p + p);
+    const unsigned long long* bp = base.p + (size_t)p * kRDigits;
+    switch (cfg) {
+      case 0:
+        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_radix_pass<K, 512, 8><<<(unsigned)tiles, 512, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
+        break;
+      case 1:
+        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_radix_pass<K, 256, 8><<<(unsigned)tiles, 256, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
+        break;
+      case 2:
+        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_radix_pass<K, 256, 16><<<(unsigned)tiles, 256, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
+        break;
+      default:
+        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_radix_pass<K, 1024, 8><<<(unsigned)tiles, 1024, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
+        break;
+    }
     EH_LAUNCH("k_radix_pass");
     K* t = src; src = dst; dst = t;
   }
