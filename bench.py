@@ -112,11 +112,16 @@ class ClockSampler:
 
 
 def _dist():
+    """(dist, rank, world_size, local_rank).  One process per GPU under torchrun;
+    the process group only carries the barrier and the max-over-ranks time
+    (replicas only: no data-path collective).  NCCL on GPUs, gloo otherwise."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
         if not dist.is_initialized():
-            dist.init_process_group("nccl")
+            backend = os.environ.get("BENCH_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+            dist.init_process_group(backend)
         return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
     return None, 0, 1, 0
 
@@ -128,6 +133,14 @@ def _max_over_ranks(dist, val: float, device) -> float:
     t = torch.tensor([val], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def aggregate(dist, ws: int, n_in_per_rank: int, local_ms: float, device="cpu"):
+    """Whole-job throughput of `ws` independent replicas: every rank processed
+    n_in_per_rank input edges in local_ms; the job took the slowest rank's time.
+    Returns (value in input edges/s, max ms)."""
+    mx = _max_over_ranks(dist, local_ms, device)
+    return ws * n_in_per_rank / (mx / 1e3), mx
 
 
 def _traffic():
@@ -278,11 +291,10 @@ def run_gpu(args, cfg, src, dst, n_in):
     mean_step = statistics.mean(step_ms)
     mean_count = statistics.mean(count_ms)
     mean_e2e = statistics.mean(e2e_ms)
-    mean_step_max = _max_over_ranks(dist, mean_step, dev)
-    mean_e2e_max = _max_over_ranks(dist, mean_e2e, dev)
+    value, mean_step_max = aggregate(dist, ws, n_in, mean_step, dev)
+    e2e_value, mean_e2e_max = aggregate(dist, ws, n_in, mean_e2e, dev)
     if rank != 0:
         return
-    value = ws * n_in / (mean_step_max / 1e3)
     achieved = st.alg_bytes_tri / (mean_count / 1e3) / 1e9
     line = {
         "metric": METRIC,
@@ -301,7 +313,7 @@ def run_gpu(args, cfg, src, dst, n_in):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": _traffic(), "peak_kind": peak_kind, "kernel": "k_tri_*  (eh_count_triangles)",
                      "alg_bytes_per_launch": st.alg_bytes_tri},
-        "e2e": {"value": ws * n_in / (mean_e2e_max / 1e3), "unit": "input edges/s",
+        "e2e": {"value": e2e_value, "unit": "input edges/s",
                 "h2d_bytes_per_step": 8 * n_in, "d2h_bytes_per_step": 8},
         "gpu_launches": launches,
         "clocks": clk,

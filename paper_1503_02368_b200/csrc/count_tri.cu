@@ -85,9 +85,9 @@ struct XSet {
   }
 };
 
-// Build the structure cooperatively (tid in [0, nthreads)); caller syncs afterwards.
-__device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, const uint32_t* xs, uint32_t d,
-                                           int tid, int nthreads) {
+// Choose the structure (no shared-memory writes): exact bitmap if x's span fits
+// the budget, else a hash with load <= 1/8 (<= 1/4 when the budget is tight).
+__device__ __forceinline__ XSet plan_xset(uint32_t* tab, uint32_t tab_words, const uint32_t* xs, uint32_t d) {
   XSet s;
   s.tab = tab;
   s.xs = xs;
@@ -96,25 +96,37 @@ __device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, co
   s.amax = xs[d - 1];
   const uint32_t lo = (s.amin >> 7) << 7;
   const uint64_t span_bits = (uint64_t)(((s.amax >> 7) + 1) << 7) - lo;
-  uint32_t hbits = 5;
-  while ((1u << hbits) < 4 * d) ++hbits;
+  uint32_t hbits = 5;  // smallest table >= 8d that fits the budget
+  while ((1u << hbits) < 8 * d && (2u << hbits) <= tab_words) ++hbits;
   if (span_bits <= 32ull * tab_words) {
     s.mode = kBitmap;
     s.lo = lo;
     s.nbits = (uint32_t)span_bits;
     s.hshift = s.hmask = 0;
-    for (uint32_t k = tid; k < s.nbits / 32; k += nthreads) tab[k] = 0u;
-  } else if ((1u << hbits) <= tab_words) {
+  } else if ((1u << hbits) <= tab_words && (1u << hbits) >= 2 * d) {
     s.mode = kHash;
     s.lo = s.nbits = 0;
     s.hshift = 32 - hbits;
     s.hmask = (1u << hbits) - 1u;
-    for (uint32_t k = tid; k < (1u << hbits); k += nthreads) tab[k] = kEmpty;
   } else {
     s.mode = kSorted;
     s.lo = s.nbits = s.hshift = s.hmask = 0;
   }
+  return s;
+}
+
+// Fill the planned structure cooperatively (tid in [0, nthreads)); caller syncs afterwards.
+__device__ __forceinline__ void fill_xset(const XSet& s, int tid, int nthreads) {
+  uint32_t* tab = s.tab;
+  const uint32_t* xs = s.xs;
+  const uint32_t d = s.d;
+  if (s.mode == kBitmap) {
+    for (uint32_t k = tid; k < s.nbits / 32; k += nthreads) tab[k] = 0u;
+  } else if (s.mode == kHash) {
+    for (uint32_t k = tid; k <= s.hmask; k += nthreads) tab[k] = kEmpty;
+  }
   if (nthreads == 32) __syncwarp(); else __syncthreads();
+  const uint32_t lo = s.lo;
   if (s.mode == kBitmap) {
     for (uint32_t k = tid; k < d; k += nthreads) {
       const uint32_t o = xs[k] - lo;
@@ -127,6 +139,12 @@ __device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, co
       while (atomicCAS(&tab[h], kEmpty, e) != kEmpty) h = (h + 1) & s.hmask;
     }
   }
+}
+
+__device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, const uint32_t* xs, uint32_t d,
+                                           int tid, int nthreads) {
+  const XSet s = plan_xset(tab, tab_words, xs, d);
+  fill_xset(s, tid, nthreads);
   return s;
 }
 
@@ -224,13 +242,17 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
     for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
     __syncwarp();
-    const XSet X = build_xset(sm.tab, kWarpBmWords, sm.xs, d, lane, 32);
+    const XSet X = plan_xset(sm.tab, kWarpBmWords, sm.xs, d);
     const uint32_t nrows = d - 1;
+    bool need_x = false;  // only AND and STREAM rows read x's staged structure
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
+      const uint8_t kd = row_kind(y, nrows - i, X);
       sm.yi[i] = y;
-      sm.kind[i] = row_kind(y, nrows - i, X);
+      sm.kind[i] = kd;
+      need_x |= (kd == kAnd || kd == kStream);
     }
+    if (__any_sync(kFull, need_x)) fill_xset(X, lane, 32);
     __syncwarp();
     uint32_t nr = 0;
 #pragma unroll

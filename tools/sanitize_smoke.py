@@ -1,0 +1,52 @@
+"""Small workload touching every kernel path, for compute-sanitizer (T7).
+
+Checks counts against closed forms / the oracle so a sanitizer run is also a
+parity run.  Usage: compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+"""
+import os
+import sys
+from math import comb
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_1503_02368_b200 as eh  # noqa: E402
+import synth  # noqa: E402
+
+
+def check(src, dst, **kw):
+    with eh.Graph(src, dst, **kw) as g:
+        t, k = g.count_triangles(), g.count_4cliques()
+        g.stats()
+    og = oracle.Graph(src, dst)
+    assert (t, k) == (og.count_triangles(), og.count_4cliques()), (t, k)
+    og.close()
+    return t, k
+
+
+src, dst = synth.rmat(12, 16, 3)
+check(src, dst)                                   # warp + CTA kernels, sort dedup
+check(src, dst, tau=2)                            # mostly uint rows (STREAM / SEARCH)
+check(src, dst, all_uint=True)
+check(src, dst, bin_small_max=1, bin_large_min=1)  # everything in the CTA kernels
+os.environ["EH_DEDUP"] = "hash"
+check(src, dst)
+del os.environ["EH_DEDUP"]
+ids = np.random.default_rng(1).choice(2**32 - 1, size=2**13, replace=False).astype(np.uint32)
+check(ids[src % ids.size], ids[dst % ids.size])   # dictionary path
+s, d = synth.complete(1100)                       # |N+(x)| > 1024: K4 fallback kernel
+with eh.Graph(s, d) as g:
+    assert g.count_triangles() == comb(1100, 3)
+    assert g.count_4cliques() == comb(1100, 4)
+e = np.zeros(0, np.uint32)
+with eh.Graph(e, e) as g:
+    assert g.count_triangles() == 0 and g.count_4cliques() == 0
+rng = np.random.default_rng(2)
+for t in range(200):
+    a = np.unique(rng.integers(0, int(rng.choice([100, 10**5, 2**32])), int(rng.integers(0, 3000)), dtype=np.uint64))
+    b = np.unique(rng.integers(0, int(rng.choice([100, 10**5, 2**32])), int(rng.integers(0, 3000)), dtype=np.uint64))
+    a = a.astype(np.uint32)
+    b = b.astype(np.uint32)
+    assert np.array_equal(eh.intersect(a, b), np.intersect1d(a, b))
+print("sanitize smoke ok")
