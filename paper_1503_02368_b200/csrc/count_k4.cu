@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
   uint32_t* xs = dsm_k4c;                                   // kCMaxD
   uint32_t* hkeys = xs + kCMaxD;                            // kCHash
   uint16_t* hidx = reinterpret_cast<uint16_t*>(hkeys + kCHash);  // kCHash u16
-  uint32_t* L = hkeys + kCHash + kCHash / 2;                // d * W words
+  uint32_t* L = hkeys + kCHash + kCHash / 2;                // d rows of S = W|1 words
+  uint16_t* jl_all = reinterpret_cast<uint16_t*>(L + kCMaxD * (kCMaxD / 32 + 1));  // per-warp edge lists
   __shared__ unsigned long long s_wi;
   constexpr uint32_t kGroups = kCWarps * 32 / kG;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -228,10 +229,11 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
       continue;
     }
     const uint32_t W = (d + 31) >> 5;
+    const uint32_t S = W | 1u;  // odd row stride: 32 lanes reading 32 different rows hit 32 banks
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     for (uint32_t k = threadIdx.x; k < (d + 3) / 4; k += blockDim.x)
       reinterpret_cast<uint4*>(xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
-    for (uint32_t k = threadIdx.x; k < d * W; k += blockDim.x) L[k] = 0u;
+    for (uint32_t k = threadIdx.x; k < d * S; k += blockDim.x) L[k] = 0u;
     __syncthreads();
     const LocalHash H = build_local_hash<true>(hkeys, hidx, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
@@ -241,26 +243,37 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      fill_row(k4_kind(y, nrows - i), col, bs, y, xs, d, i, H, L + i * W, gl);
+      fill_row(k4_kind(y, nrows - i), col, bs, y, xs, d, i, H, L + i * S, gl);
       i = inext;
       y = ynext;
     }
     __syncthreads();
-    // bit-parallel innermost loop: one warp per row, lane k holds word k
+    // bit-parallel innermost loop: one warp per row i; the set bits j of L_i (the
+    // local edges) are listed, then each LANE takes one edge and ANDs the words
+    // of L_i and L_j above j (broadcast read of L_i, conflict-free reads of L_j).
+    uint16_t* jl = jl_all + w * kCMaxD;
     for (uint32_t r = w; r < d; r += kCWarps) {
-      const uint32_t li = ((uint32_t)lane < W) ? L[r * W + lane] : 0u;
-      for (uint32_t kk = 0; kk < W; ++kk) {
-        uint32_t wb = __shfl_sync(kFull, li, kk);
-        while (wb) {
-          const uint32_t b = __ffs(wb) - 1;
-          wb &= wb - 1;
-          const uint32_t j = kk * 32 + b;
-          if ((uint32_t)lane >= kk && (uint32_t)lane < W) {
-            const uint32_t m = ((uint32_t)lane == kk) ? ~((2u << b) - 1u) : 0xFFFFFFFFu;
-            cnt += __popc(li & L[j * W + lane] & m);
-          }
-        }
+      const uint32_t* Li = L + r * S;
+      const uint32_t wv = ((uint32_t)lane < W) ? Li[lane] : 0u;
+      const uint32_t c = __popc(wv);
+      const uint32_t incl = warp_inclusive_scan(c);
+      const uint32_t ne = __shfl_sync(kFull, incl, 31);
+      uint32_t p = incl - c, t = wv;
+      while (t) {
+        const uint32_t b = __ffs(t) - 1;
+        t &= t - 1;
+        jl[p++] = (uint16_t)(lane * 32 + b);
       }
+      __syncwarp();
+      for (uint32_t e = lane; e < ne; e += 32) {
+        const uint32_t j = jl[e];
+        const uint32_t kk = j >> 5;
+        const uint32_t* Lj = L + j * S;
+        uint32_t acc = __popc(Li[kk] & Lj[kk] & ~((2u << (j & 31)) - 1u));
+        for (uint32_t k = kk + 1; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
+        cnt += acc;
+      }
+      __syncwarp();
     }
     __syncthreads();
   }
@@ -268,7 +281,8 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
-constexpr size_t kCtaSmemK4 = (size_t)(kCMaxD + kCHash + kCHash / 2 + kCMaxD * (kCMaxD / 32)) * 4;
+constexpr size_t kCtaSmemK4 =
+    (size_t)(kCMaxD + kCHash + kCHash / 2 + kCMaxD * (kCMaxD / 32 + 1)) * 4 + (size_t)kCWarps * kCMaxD * 2;
 
 // ------------------------------------------- fallback: |N+(x)| > kCMaxD --
 // P = N+(x) after y cap N+(y) materialised per warp (global scratch), then
