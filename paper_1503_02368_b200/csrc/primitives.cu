@@ -96,7 +96,7 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 
 // ------------------------------------------------------------- radix sort --
 constexpr int kRBlock = 256;                  // histogram kernel
-constexpr int kRadixDefaultCfg = 0;           // pass kernel tile: 512 threads x 8 keys (see radix_impl)
+constexpr int kRadixDefaultCfg = 2;           // pass kernel tile: 256 threads x 16 keys (measured best, see radix_impl)
 constexpr int kRDigits = 256;
 constexpr int kRMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long lon
 
 // (2) one pass
 template <typename K, int kPBlock, int kRItems>
-__global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+__global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
                                                         uint32_t shift, const unsigned long long* __restrict__ base,
                                                         unsigned long long* __restrict__ status,
                                                         uint32_t* __restrict__ tile_ctr) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in
   const uint64_t tn = min((uint64_t)kRTile, n - t0);
   const unsigned lt = (1u << lane) - 1u;
   K key[kRItems];
-  uint32_t rk[kRItems], dg[kRItems];
+  uint32_t rd[kRItems];  // rank within the warp sub-tile (low 16 bits) | digit << 16 (0x100: invalid)
 #pragma unroll
   for (int r = 0; r < kRItems; ++r) {
     const uint32_t li = (uint32_t)w * 32 * kRItems + (uint32_t)r * 32 + lane;
@@ -167,8 +167,7 @@ __global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in
     __syncwarp();
     if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(before + __popc(peers));
     __syncwarp();
-    rk[r] = before + __popc(peers & lt);
-    dg[r] = d;
+    rd[r] = (before + __popc(peers & lt)) | (d << 16);
   }
   __syncthreads();
   // thread d < 256: per-warp exclusive prefix, tile total, look-back
@@ -231,7 +230,7 @@ __global__ void __launch_bounds__(kPBlock) k_radix_pass(const K* __restrict__ in
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRItems; ++r)
-    if (dg[r] < 0x100u) skeys[tdp[dg[r]] + wcnt[w][dg[r]] + rk[r]] = key[r];
+    if ((rd[r] >> 16) < 0x100u) skeys[tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu)] = key[r];
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < tn; i += kPBlock) {
     const K k = skeys[i];
