@@ -111,7 +111,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
         EH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
       }
       eh::PhaseTimer timer(g->stream);
-      g->d_counter = (unsigned long long*)g->own(4 * sizeof(unsigned long long));
+      g->d_counter = (unsigned long long*)g->own(8 * sizeof(unsigned long long));
       timer.mark("alloc");
       // a1: upload (borrowed inputs are copied)
       eh::DBuf<uint32_t> in;

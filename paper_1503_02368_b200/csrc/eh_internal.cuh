@@ -210,7 +210,7 @@ struct eh_graph {
   // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
   uint32_t* work = nullptr;
   uint64_t n_work[3] = {0, 0, 0};
-  unsigned long long* d_counter = nullptr;  // 2 x u64 accumulators
+  unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
 
   std::vector<void*> owned;  // every device allocation above
