@@ -51,6 +51,12 @@ def _load():
         lib.oracle_triangles_at.restype = ctypes.c_uint64
         lib.oracle_intersect.argtypes = [u32p, ctypes.c_uint64, u32p, ctypes.c_uint64, u32p]
         lib.oracle_intersect.restype = ctypes.c_int64
+        lib.oracle_triangles_per_vertex.argtypes = [vp, u64p]
+        lib.oracle_triangles_per_vertex.restype = None
+        for name in ("oracle_count_lollipop", "oracle_count_barbell"):
+            f = getattr(lib, name)
+            f.argtypes = [vp, u64p]
+            f.restype = ctypes.c_int
         lib.oracle_stats.argtypes = [vp, u64p]
         lib.oracle_stats.restype = None
         lib.oracle_export.argtypes = [vp, u32p, u32p, u64p, u32p]
@@ -110,6 +116,26 @@ class Graph:
 
     def triangles_at(self, x: int) -> int:
         return int(_load().oracle_triangles_at(self._h, x))
+
+    def triangles_per_vertex(self) -> np.ndarray:
+        """t(v) = number of triangles containing v, for v = vid[i] (sorted original ids)."""
+        t = np.empty(max(self.n_vertices, 1), np.uint64)
+        _load().oracle_triangles_per_vertex(self._h, t.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+        return t[:self.n_vertices]
+
+    def _count128(self, fn) -> int:
+        out = (ctypes.c_uint64 * 2)()
+        if fn(self._h, out) != 0:
+            raise MemoryError("oracle allocation failed")
+        return int(out[0]) | (int(out[1]) << 64)
+
+    def count_lollipop(self) -> int:
+        """COUNT(*) of Lollipop L3,1 on the undirected data."""
+        return self._count128(_load().oracle_count_lollipop)
+
+    def count_barbell(self) -> int:
+        """COUNT(*) of Barbell B3,1 on the undirected data."""
+        return self._count128(_load().oracle_count_barbell)
 
     def export(self):
         """(vid, deg, off, adj): sorted original ids, degrees, out-list offsets,

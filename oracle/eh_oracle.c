@@ -289,6 +289,75 @@ uint64_t oracle_triangles_at(const oracle_graph* g, uint32_t x) {
   return tri_range(g, i, i + 1);
 }
 
+/*
+ * NEXT-1: Lollipop L3,1 and Barbell B3,1 COUNT(*) by the
+ * paper's two-phase GHD plan (PAPER.md:379-416 Example `ex:barbell`,
+ * PAPER.md:545-567 "Across Nodes": Yannakakis bottom-up pass).  Both queries
+ * run on the UNDIRECTED (symmetric) data:
+ *   Lollipop(x,y,z,w) :- R(x,y),S(y,z),T(x,z),U(x,w).
+ *   Barbell(x,y,z,x',y',z') :- R(x,y),S(y,z),T(x,z),U(x,x'),R'(x',y'),
+ *                              S'(y',z'),T'(x',z').
+ * Child GHD node {x,y,z}: the triangle nest, aggregated (COUNT) and projected
+ * onto x -- on symmetric data every triangle containing x yields the 2 ordered
+ * bindings (y,z), so the projected count is 2 t(x), t(x) = #triangles with x.
+ * Root node: Lollipop joins it with U(x,w): sum_x 2 t(x) deg(x); Barbell joins
+ * the two children through U(x,x'): sum over ORDERED edges (x,x') of
+ * (2 t(x)) (2 t(x')).  Counts can exceed 2^64 (Barbell), so they are returned
+ * as 128-bit values (lo, hi).
+ */
+
+/* t(v) for every vertex index: each triangle x<y<z of the oriented nest adds 1
+ * to x, y and z (the merge reports the matching z). */
+void oracle_triangles_per_vertex(const oracle_graph* g, uint64_t* t) {
+  memset(t, 0, g->nv * sizeof(uint64_t));
+  uint32_t* P = (uint32_t*)malloc((g->max_out ? g->max_out : 1) * sizeof(uint32_t));
+  if (!P) return;
+  for (uint64_t x = 0; x < g->nv; ++x) {
+    if (DOUT(g, x) == 0) continue;
+    for (uint64_t e = g->off[x]; e < g->off[x + 1]; ++e) {
+      const uint64_t y = vindex(g, g->adj[e]);
+      if (DOUT(g, y) == 0) continue;
+      const uint64_t np = merge_into(OUT(g, y), DOUT(g, y), OUT(g, x), DOUT(g, x), P);
+      t[x] += np;
+      t[y] += np;
+      for (uint64_t k = 0; k < np; ++k) t[vindex(g, P[k])] += 1;
+    }
+  }
+  free(P);
+}
+
+static void add128(uint64_t* lo, uint64_t* hi, unsigned __int128 v) {
+  unsigned __int128 s = ((unsigned __int128)*hi << 64 | *lo) + v;
+  *lo = (uint64_t)s;
+  *hi = (uint64_t)(s >> 64);
+}
+
+/* out2 = {lo, hi} of the Lollipop COUNT(*); returns 0 or -1 on allocation failure. */
+int oracle_count_lollipop(const oracle_graph* g, uint64_t* out2) {
+  uint64_t* t = (uint64_t*)malloc((g->nv ? g->nv : 1) * sizeof(uint64_t));
+  if (!t) return -1;
+  oracle_triangles_per_vertex(g, t);
+  out2[0] = out2[1] = 0;
+  for (uint64_t x = 0; x < g->nv; ++x) add128(&out2[0], &out2[1], (unsigned __int128)2 * t[x] * g->deg[x]);
+  free(t);
+  return 0;
+}
+
+int oracle_count_barbell(const oracle_graph* g, uint64_t* out2) {
+  uint64_t* t = (uint64_t*)malloc((g->nv ? g->nv : 1) * sizeof(uint64_t));
+  if (!t) return -1;
+  oracle_triangles_per_vertex(g, t);
+  out2[0] = out2[1] = 0;
+  /* each undirected edge {x, x'} appears once in E+ and twice as an ordered pair */
+  for (uint64_t x = 0; x < g->nv; ++x)
+    for (uint64_t e = g->off[x]; e < g->off[x + 1]; ++e) {
+      const uint64_t y = vindex(g, g->adj[e]);
+      add128(&out2[0], &out2[1], (unsigned __int128)8 * t[x] * t[y]);
+    }
+  free(t);
+  return 0;
+}
+
 /* stats: [n_input, m, nv, max_out] */
 void oracle_stats(const oracle_graph* g, uint64_t* out4) {
   out4[0] = g->n_input; out4[1] = g->m; out4[2] = g->nv; out4[3] = g->max_out;

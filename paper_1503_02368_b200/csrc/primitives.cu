@@ -258,7 +258,7 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& 
   // tile shape (threads x keys per thread); EH_RADIX_CFG selects one for tuning
   static const int cfg_env = [] { const char* e = getenv("EH_RADIX_CFG"); return e ? atoi(e) : -1; }();
   const int cfg = (cfg_env >= 0 && cfg_env <= 3) ? cfg_env : kRadixDefaultCfg;
-  static const int kThreads[4] = {512, 256, 256, 1024}, kItems[4] = {8, 8, 16, 8};
+  static const int kThreads[4] = {512, 256, 256, 512}, kItems[4] = {8, 8, 16, 16};
   const uint64_t tile = (uint64_t)kThreads[cfg] * kItems[cfg];
   const uint64_t tiles = (n + tile - 1) / tile;
   if (tiles >= (1ull << 31)) fail(EH_EINVAL, "radix sort: too many keys");
@@ -284,8 +284,8 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& 
         k_radix_pass<K, 256, 16><<<(unsigned)tiles, 256, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
         break;
       default:
-        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_radix_pass<K, 1024, 8><<<(unsigned)tiles, 1024, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
+        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 512, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_radix_pass<K, 512, 16><<<(unsigned)tiles, 512, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
         break;
     }
     EH_LAUNCH("k_radix_pass");

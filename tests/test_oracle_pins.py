@@ -276,3 +276,55 @@ def test_triangles_at_sums_to_total():
     assert sum(g.triangles_at(int(v)) for v in vid) == g.count_triangles(2)
     assert g.count_triangles_range(0, vid.size // 2, 2) + g.count_triangles_range(vid.size // 2, vid.size, 3) \
         == g.count_triangles(1)
+
+
+# ------------------------------------------------- NEXT-1: Lollipop / Barbell --
+def _ordered_triangles(A):
+    n = A.shape[0]
+    return [(x, y, z) for x in range(n) for y in range(n) for z in range(n) if A[x, y] and A[y, z] and A[x, z]]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_per_vertex_triangles_and_lollipop_barbell_vs_literal_join(seed):
+    """Literal evaluation of the paper's queries over the SYMMETRIC relation
+    (PAPER.md:227, 234, 877-878): every satisfying ordered tuple counted."""
+    import itertools
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(4, 11))
+    src, dst = synth.random_graph(n, int(rng.integers(n, n * n)), seed)
+    A = B.adjacency(src, dst)
+    g = oracle.Graph(src, dst)
+    vid, *_ = g.export()
+    ids = np.unique(np.concatenate([src, dst]).astype(np.int64))  # adjacency() compacts ids the same way
+    pos = {int(v): i for i, v in enumerate(ids)}
+    t_brute = [sum(1 for a, b in itertools.combinations(range(A.shape[0]), 2)
+                   if A[v, a] and A[v, b] and A[a, b]) for v in range(A.shape[0])]
+    t = g.triangles_per_vertex()
+    for i, v in enumerate(vid):
+        assert t[i] == t_brute[pos[int(v)]]
+    assert int(t.sum()) == 3 * g.count_triangles(1)
+    m = A.shape[0]
+    lolli = sum(1 for x, y, z, w in itertools.product(range(m), repeat=4)
+                if A[x, y] and A[y, z] and A[x, z] and A[x, w])
+    assert g.count_lollipop() == lolli
+    tri = _ordered_triangles(A)
+    xs = np.array([p[0] for p in tri], dtype=np.int64)
+    barb = int(A[np.ix_(xs, xs)].sum()) if xs.size else 0
+    assert g.count_barbell() == barb
+
+
+@pytest.mark.parametrize("n", [3, 4, 7, 30])
+def test_lollipop_barbell_closed_forms_kn(n):
+    g = oracle.Graph(*synth.complete(n))
+    t = comb(n - 1, 2)
+    assert np.all(g.triangles_per_vertex() == t)
+    assert g.count_lollipop() == n * 2 * t * (n - 1)
+    assert g.count_barbell() == n * (n - 1) * (2 * t) ** 2
+
+
+def test_barbell_exceeds_u64_is_exact():
+    # K_1630: Barbell = n(n-1)(2 C(n-1,2))^2 = 1.012 * 2^64 -> needs the 128-bit result
+    n = 1630
+    g = oracle.Graph(*synth.complete(n))
+    val = n * (n - 1) * (2 * comb(n - 1, 2)) ** 2
+    assert val > 2**64 and g.count_barbell() == val
