@@ -120,6 +120,32 @@ uint64_t eh_count_triangles(eh_graph* g);
 uint64_t eh_count_4cliques(eh_graph* g);
 
 /*
+ * eh_triangles_per_vertex -- t(v) = the number of triangles containing v, for
+ * every non-isolated vertex: the GROUP BY x aggregate
+ * of the triangle node of the Lollipop/Barbell GHDs (Example `ex:barbell`,
+ * PAPER.md:379-416, bottom-up pass PAPER.md:545-567; per x the projection
+ * counts 2 t(x) ordered (y, z) pairs on symmetric data).
+ *  t [n_active] : caller-owned uint64, host memory or device memory of g's
+ *                 device (detected); t[r] belongs to the vertex of rank r,
+ *                 whose original id is eh_graph_export's orig_id[r].
+ * Returns EH_OK, EH_EINVAL (NULL argument, output on another device), EH_ENOMEM, EH_ECUDA.
+ */
+int eh_triangles_per_vertex(eh_graph* g, uint64_t* t);
+
+/*
+ * eh_count_lollipop / eh_count_barbell -- COUNT(*) of
+ *   Lollipop(x,y,z,w) :- R(x,y),S(y,z),T(x,z),U(x,w).
+ *   Barbell(x,y,z,x',y',z') :- R(x,y),S(y,z),T(x,z),U(x,x'),R'(x',y'),S'(y',z'),T'(x',z').
+ * on the UNDIRECTED (symmetric) Edge relation, as the paper runs them
+ * (PAPER.md:877-878), by the two-phase GHD plan: L3,1 = sum_v 2 t(v) deg(v),
+ * B3,1 = sum over ordered edges (x, x') of 2 t(x) 2 t(x').  The counts can
+ * exceed 2^64, so out[0] / out[1] receive the low / high 64 bits (host memory).
+ * Returns EH_OK, EH_EINVAL (NULL argument), EH_ENOMEM, EH_ECUDA.
+ */
+int eh_count_lollipop(eh_graph* g, uint64_t out[2]);
+int eh_count_barbell(eh_graph* g, uint64_t out[2]);
+
+/*
  * eh_intersect -- the set operation "xs cap ys" of Table `lst:eh_operators`
  * (PAPER.md:515-516), with the paper's layout-dependent algorithms
  * (PAPER.md:628-642): each input gets the set-level layout (uint or bitset,

@@ -161,6 +161,41 @@ uint64_t eh_count_4cliques(eh_graph* g) {
   });
 }
 
+int eh_triangles_per_vertex(eh_graph* g, uint64_t* t) {
+  return guarded<int>(EH_ECUDA, [&]() -> int {
+    if (!g || (!t && g->n_act)) eh::fail(EH_EINVAL, "eh_triangles_per_vertex: NULL argument");
+    DeviceGuard guard(g->device);
+    if (g->n_act == 0) return EH_OK;
+    cudaPointerAttributes pa{};
+    EH_CUDA(cudaPointerGetAttributes(&pa, t));
+    const bool on_device = pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged;
+    if (on_device && pa.device != g->device)
+      eh::fail(EH_EINVAL, "eh_triangles_per_vertex: output on device %d, graph on device %d", pa.device, g->device);
+    if (on_device) {
+      eh::triangles_per_vertex(g, reinterpret_cast<unsigned long long*>(t));
+      EH_CUDA(cudaStreamSynchronize(g->stream));
+    } else {
+      eh::DBuf<unsigned long long> d(g->alloc, g->n_act);
+      eh::triangles_per_vertex(g, d.p);
+      EH_CUDA(cudaMemcpyAsync(t, d.p, g->n_act * 8, cudaMemcpyDeviceToHost, g->stream));
+      EH_CUDA(cudaStreamSynchronize(g->stream));
+    }
+    return EH_OK;
+  });
+}
+
+static int count128(eh_graph* g, uint64_t* out, bool barbell, const char* what) {
+  return guarded<int>(EH_ECUDA, [&]() -> int {
+    if (!g || !out) eh::fail(EH_EINVAL, "%s: NULL argument", what);
+    DeviceGuard guard(g->device);
+    eh::count_lollipop_barbell(g, barbell, out);
+    return EH_OK;
+  });
+}
+
+int eh_count_lollipop(eh_graph* g, uint64_t out[2]) { return count128(g, out, false, "eh_count_lollipop"); }
+int eh_count_barbell(eh_graph* g, uint64_t out[2]) { return count128(g, out, true, "eh_count_barbell"); }
+
 int64_t eh_intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out) {
   int64_t r = guarded<int64_t>(INT64_MIN, [&]() -> int64_t { return eh::intersect(a, na, b, nb, out); });
   return r == INT64_MIN ? (int64_t)t_status : r;

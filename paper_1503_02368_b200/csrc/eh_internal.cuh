@@ -205,6 +205,7 @@ struct eh_graph {
   uint32_t* col = nullptr;      // padded per list to 4 elements with kNone
   uint32_t* bs = nullptr;       // bitset pool (128-bit aligned chunks at absolute id/128)
   uint32_t* orig_id = nullptr;  // original id of each rank
+  uint32_t* deg_rank = nullptr; // degree (distinct neighbours) of each rank
   uint32_t* bytes32 = nullptr;  // bytes(N+(v)) at tau = 32 (B_tri accounting)
   bool stats_ready = false;
   // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
@@ -235,6 +236,9 @@ void build_worklists(eh_graph* g);
 uint64_t count_triangles(eh_graph* g);
 uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept
 uint64_t count_4cliques(eh_graph* g);
+// count_pv.cu (NEXT-1): t(v) per rank into a device array; Lollipop / Barbell 128-bit counts
+void triangles_per_vertex(eh_graph* g, unsigned long long* d_t);
+void count_lollipop_barbell(eh_graph* g, bool barbell, uint64_t out2[2]);
 // intersect.cu
 int64_t intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);
 }  // namespace eh

@@ -151,12 +151,14 @@ struct RankKeyEmit {  // (deg << b) | id, sorted ascending = the (degree, id) or
 };
 
 __global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint32_t b, uint32_t* __restrict__ rank,
-                       uint32_t* __restrict__ orig, const uint32_t* __restrict__ dict) {
+                       uint32_t* __restrict__ orig, const uint32_t* __restrict__ dict, uint32_t* __restrict__ deg_rank) {
   const uint64_t mask = (1ull << b) - 1ull;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_act; r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t id = (uint32_t)(sorted[r] & mask);
+    const uint64_t key = sorted[r];
+    const uint32_t id = (uint32_t)(key & mask);
     rank[id] = (uint32_t)r;
     orig[r] = dict ? dict[id] : id;
+    deg_rank[r] = (uint32_t)(key >> b);  // the key is (deg << b) | id
   }
 }
 
@@ -311,8 +313,9 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + bitlen(max_deg), al, s);
   DBuf<uint32_t>& rank = deg;  // reuse: the degree of every active id is already encoded in rkeys
   g->orig_id = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);
+  g->deg_rank = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);
   if (n_act) {
-    k_rank<<<grid_for(n_act, TB * 4), TB, 0, s>>>(rsorted, n_act, b, rank.p, g->orig_id, dict.p);
+    k_rank<<<grid_for(n_act, TB * 4), TB, 0, s>>>(rsorted, n_act, b, rank.p, g->orig_id, dict.p, g->deg_rank);
     EH_LAUNCH("k_rank");
   }
   rkeys.reset();

@@ -67,6 +67,11 @@ def lib():
         L.eh_count_triangles.restype = u64
         L.eh_count_4cliques.argtypes = [vp]
         L.eh_count_4cliques.restype = u64
+        L.eh_triangles_per_vertex.argtypes = [vp, vp]
+        L.eh_triangles_per_vertex.restype = ctypes.c_int
+        for name in ("eh_count_lollipop", "eh_count_barbell"):
+            getattr(L, name).argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+            getattr(L, name).restype = ctypes.c_int
         L.eh_intersect.argtypes = [u32p, u64, u32p, u64, u32p]
         L.eh_intersect.restype = ctypes.c_int64
         L.eh_graph_stats.argtypes = [vp, ctypes.POINTER(EHStats)]
@@ -86,7 +91,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("eh_load_edges", "eh_load_edges_ex", "eh_count_triangles", "eh_count_4cliques",
-                    "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
+                    "eh_triangles_per_vertex", "eh_count_lollipop", "eh_count_barbell", "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
                     "eh_last_error")
 
 
@@ -209,6 +214,37 @@ class Graph:
         if r == EH_COUNT_ERROR:
             _raise()
         return int(r)
+
+    def triangles_per_vertex(self, out=None):
+        """t(v) per rank (eh_triangles_per_vertex); rank r is original id export()[2][r].
+
+        ``out``: optional uint64/int64 CUDA tensor of n_active elements (filled on the
+        device); otherwise a host numpy uint64 array is returned."""
+        n = self.stats().n_active
+        if out is None:
+            t = np.zeros(max(n, 1), np.uint64)
+            ptr = t.ctypes.data
+        else:
+            if out.numel() < n:
+                raise ValueError(f"out has {out.numel()} elements, need {n}")
+            t, ptr = out, out.data_ptr()
+        if lib().eh_triangles_per_vertex(self._h, ptr) != EH_OK:
+            _raise()
+        return t[:n]
+
+    def _count128(self, fn) -> int:
+        out = (ctypes.c_uint64 * 2)()
+        if fn(self._h, out) != EH_OK:
+            _raise()
+        return int(out[0]) | (int(out[1]) << 64)
+
+    def count_lollipop(self) -> int:
+        """COUNT(*) of Lollipop L3,1 on the undirected data (eh_count_lollipop), exact (128-bit)."""
+        return self._count128(lib().eh_count_lollipop)
+
+    def count_barbell(self) -> int:
+        """COUNT(*) of Barbell B3,1 on the undirected data (eh_count_barbell), exact (128-bit)."""
+        return self._count128(lib().eh_count_barbell)
 
     def stats(self) -> Stats:
         st = EHStats()
