@@ -11,13 +11,17 @@
 //   L3,1 = sum_x 2 t(x) deg(x)        B3,1 = sum over ordered edges (x,x') of 2 t(x) * 2 t(x')
 // The counts can exceed 2^64, so they are accumulated in 128 bits.
 //
-// t(v): the oriented triangle nest of count_tri.cu with
-// every found triangle x<y<z credited to its three vertices.  x gets its row
-// sums, y gets one atomic per row, and z is credited through a per-x shared
-// counter indexed by z's LOCAL position in N+(x) (z is always in N+(x)), flushed
-// once per x -- so hub vertices do not serialise one global atomic per triangle.
-// Rows use the uint cap bitset probe, the galloping binary search, or a stream
-// of N+(y) against a shared-memory hash of N+(x) that returns the local index.
+// t(v): the oriented triangle nest of count_tri.cu (its row
+// kinds PROBE / STREAM / SEARCH, same work classes) with every found triangle
+// x<y<z credited to its three vertices.  y and z are both elements of
+// N+(x), so their credits go to a per-x shared-memory counter indexed by the
+// LOCAL position in N+(x) (row totals for y, one increment per hit for z), and
+// are flushed with one global atomic per element of N+(x); x gets its row sum.
+// The membership structure of x therefore also returns that position: an exact
+// bitmap plus, per 32-bit word, the position of its first element (positions
+// within a word by popcount), or a hash table with a position per slot, or a
+// binary search of the sorted list.  (No AND rows: see row_kind.)  Tuned on
+// C2-C4 (DESIGN.md NEXT-1): 8-warp CTAs with 28 KB of shared memory, 8 per SM.
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "rows.cuh"
@@ -27,94 +31,161 @@ namespace eh {
 namespace {
 
 constexpr int kG = 8;
-constexpr int kPvWarpMaxD = 128;  // must equal tri_warp_max_degree(): the work classes are shared
-constexpr int kPvWHash = 512;     // >= 4 d
-constexpr int kPvWarps = 8;
-constexpr int kPvCtaXCap = 4096;
-constexpr int kPvCHash = 16384;   // >= 4 d
-constexpr int kPvCtaWarps = 16;
-constexpr uint32_t kEmptyP = 0xFFFFFFFFu;
+constexpr int kWarpMaxD = 128;       // must equal tri_warp_max_degree(): the work classes are shared
+constexpr int kWarpTabWords = 256;   // warp-kernel x structure: bitmap of 8192 ids or 256-slot hash
+constexpr int kWarps = 8;
+constexpr int kCtaWarps = 8;
+constexpr uint32_t kCtaXCapMin = 2048;    // N+(x) staged (and counted locally) up to xcap >= this size:
+constexpr uint32_t kCtaXCapMax = 16384;   // xcap = max |N+(x)| rounded up to a power of two, clamped
+constexpr int kCtaTabWords = 2048;   // CTA x structure: bitmap of 65536 ids, or a hash of <= 2048 slots
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
-struct IdxHash {  // N+(x) -> local index; idx == nullptr: binary search in xs instead
-  const uint32_t* keys;
-  const uint16_t* idx;
+enum RowKind : uint8_t { kSkip = 0, kProbe = 1, kStream = 2, kSearch = 3 };
+enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2 };
+
+// N+(x) with local positions.  Bitmap: pos[w] = position of the first element
+// in word w (only read for words that hold an element).  Hash: pos[slot].
+struct XIdx {
+  uint32_t* tab;
+  uint16_t* pos;
   const uint32_t* xs;
-  uint32_t d, shift, mask, amin, amax;
-  __device__ __forceinline__ int lookup(uint32_t e) const {
+  uint32_t mode, lo, nbits, hshift, hmask, d, amin, amax;
+
+  __device__ __forceinline__ int index_of(uint32_t e) const {
+    if (mode == kBitmap) {
+      const uint32_t o = e - lo;
+      if (o >= nbits) return -1;
+      const uint32_t w = tab[o >> 5], b = o & 31;
+      if (!((w >> b) & 1u)) return -1;
+      return pos[o >> 5] + __popc(w & ((1u << b) - 1u));
+    }
     if (e < amin || e > amax) return -1;
-    if (idx) {
-      uint32_t s = (e * 2654435761u) >> shift;
+    if (mode == kHash) {
+      uint32_t s = (e * 2654435761u) >> hshift;
       for (;;) {
-        const uint32_t v = keys[s];
-        if (v == e) return idx[s];
-        if (v == kEmptyP) return -1;
-        s = (s + 1) & mask;
+        const uint32_t v = tab[s];
+        if (v == e) return pos[s];
+        if (v == kEmpty) return -1;
+        s = (s + 1) & hmask;
       }
     }
-    uint32_t lo = 0, len = d;
+    uint32_t l = 0, len = d;
     while (len > 0) {
       const uint32_t h = len >> 1;
-      if (xs[lo + h] < e) { lo += h + 1; len -= h + 1; } else { len = h; }
+      if (xs[l + h] < e) { l += h + 1; len -= h + 1; } else { len = h; }
     }
-    return (lo < d && xs[lo] == e) ? (int)lo : -1;
+    return (l < d && xs[l] == e) ? (int)l : -1;
   }
 };
 
-template <bool kCta>
-__device__ __forceinline__ IdxHash build_idx_hash(uint32_t* keys, uint16_t* idx, const uint32_t* xs, uint32_t d,
-                                                  bool staged, int tid, int nt) {
-  IdxHash H{keys, staged ? idx : nullptr, xs, d, 0, 0, xs[0], xs[d - 1]};
-  if (!staged) return H;
+__device__ __forceinline__ XIdx plan_x(uint32_t* tab, uint16_t* pos, uint32_t tab_words, const uint32_t* xs,
+                                       uint32_t d) {
+  XIdx s;
+  s.tab = tab;
+  s.pos = pos;
+  s.xs = xs;
+  s.d = d;
+  s.amin = xs[0];
+  s.amax = xs[d - 1];
+  const uint32_t lo = (s.amin >> 7) << 7;
+  const uint64_t span_bits = (uint64_t)(((s.amax >> 7) + 1) << 7) - lo;
   uint32_t hbits = 5;
-  while ((1u << hbits) < 4 * d) ++hbits;
-  H.shift = 32 - hbits;
-  H.mask = (1u << hbits) - 1u;
-  for (uint32_t k = tid; k <= H.mask; k += nt) keys[k] = kEmptyP;
-  if (kCta) __syncthreads(); else __syncwarp();
-  for (uint32_t k = tid; k < d; k += nt) {
-    const uint32_t e = xs[k];
-    uint32_t h = (e * 2654435761u) >> H.shift;
-    while (atomicCAS(&keys[h], kEmptyP, e) != kEmptyP) h = (h + 1) & H.mask;
-    idx[h] = (uint16_t)k;
+  while ((1u << hbits) < 8 * d && (2u << hbits) <= tab_words) ++hbits;
+  s.lo = s.nbits = s.hshift = s.hmask = 0;
+  if (span_bits <= 32ull * tab_words) {
+    s.mode = kBitmap;
+    s.lo = lo;
+    s.nbits = (uint32_t)span_bits;
+  } else if ((1u << hbits) <= tab_words && (1u << hbits) >= 2 * d) {
+    s.mode = kHash;
+    s.hshift = 32 - hbits;
+    s.hmask = (1u << hbits) - 1u;
+  } else {
+    s.mode = kSorted;
   }
-  return H;
+  return s;
 }
 
-// Credit one hit z = x_j: local counter if staged, else a direct global atomic.
+template <bool kCta>
+__device__ __forceinline__ void fill_x(const XIdx& s, int tid, int nt) {
+  if (s.mode == kBitmap) {
+    for (uint32_t k = tid; k < s.nbits / 32; k += nt) s.tab[k] = 0u;
+  } else if (s.mode == kHash) {
+    for (uint32_t k = tid; k <= s.hmask; k += nt) s.tab[k] = kEmpty;
+  }
+  if (kCta) __syncthreads(); else __syncwarp();
+  if (s.mode == kBitmap) {
+    for (uint32_t k = tid; k < s.d; k += nt) {
+      const uint32_t o = s.xs[k] - s.lo;
+      atomicOr(&s.tab[o >> 5], 1u << (o & 31));
+      if (k == 0 || ((s.xs[k - 1] - s.lo) >> 5) != (o >> 5)) s.pos[o >> 5] = (uint16_t)k;  // xs sorted
+    }
+  } else if (s.mode == kHash) {
+    for (uint32_t k = tid; k < s.d; k += nt) {
+      const uint32_t e = s.xs[k];
+      uint32_t h = (e * 2654435761u) >> s.hshift;
+      while (atomicCAS(&s.tab[h], kEmpty, e) != kEmpty) h = (h + 1) & s.hmask;
+      s.pos[h] = (uint16_t)k;
+    }
+  }
+}
+
+// Row kinds as count_tri.cu minus AND: a row whose N+(y) is a bitset is PROBEd
+// element by element, because every hit must be attributed to its z, and
+// extracting the set bits of ANDed chunks measured slower on B200 than probing
+// (DESIGN.md NEXT-1).  Rows whose bitset span misses x's span are skipped.
+__device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XIdx& X) {
+  if (a == 0 || y.len == 0) return kSkip;
+  if (y.c1 > y.c0) {
+    if (y.c1 <= (X.amin >> 7) || y.c0 > (X.amax >> 7)) return kSkip;
+    return kProbe;
+  }
+  const uint32_t lg = 32 - __clz(y.len);
+  if ((uint64_t)a * lg * 4 < y.len) return kSearch;
+  return kStream;
+}
+
+// Credit one hit z = N+(x)[j]: local counter if N+(x) is staged, else a global atomic.
 __device__ __forceinline__ void credit(uint32_t* lc, unsigned long long* t, const uint32_t* xs, int j) {
   if (lc) atomicAdd(&lc[j], 1u);
   else atomicAdd(&t[xs[j]], 1ull);
 }
 
-// Row (x, y) with y = xs[i] on an 8-lane group; returns this lane's hit count.
-__device__ __forceinline__ uint32_t pv_row(const YInfo& y, const uint32_t* xs, uint32_t d, uint32_t i,
-                                           const IdxHash& H, uint32_t* lc, unsigned long long* t,
-                                           const uint32_t* __restrict__ col, const uint32_t* __restrict__ bs,
-                                           uint32_t gl) {
-  const uint32_t a = d - 1 - i;
+// Row (x, y = xs[i]) on an 8-lane group; returns this lane's hit count.
+__device__ __forceinline__ uint32_t pv_row(uint8_t kd, const YInfo& y, const XIdx& X, uint32_t i, uint32_t* lc,
+                                           unsigned long long* t, const uint32_t* __restrict__ col,
+                                           const uint32_t* __restrict__ bs, uint32_t gl) {
+  const uint32_t* xs = X.xs;
+  const uint32_t d = X.d;
   uint32_t c = 0;
-  if (a == 0 || y.len == 0) return 0;
-  if (y.c1 > y.c0) {  // uint cap bitset probe
-    for (uint32_t j = i + 1 + gl; j < d; j += kG)
+  if (kd == kProbe) {  // 4 probes in flight per lane
+    uint32_t j = i + 1 + gl;
+    for (; j + 3 * kG < d; j += 4 * kG) {
+      const uint32_t h0 = probe_bits(bs, y, xs[j]), h1 = probe_bits(bs, y, xs[j + kG]);
+      const uint32_t h2 = probe_bits(bs, y, xs[j + 2 * kG]), h3 = probe_bits(bs, y, xs[j + 3 * kG]);
+      if (h0) credit(lc, t, xs, (int)j);
+      if (h1) credit(lc, t, xs, (int)(j + kG));
+      if (h2) credit(lc, t, xs, (int)(j + 2 * kG));
+      if (h3) credit(lc, t, xs, (int)(j + 3 * kG));
+      c += h0 + h1 + h2 + h3;
+    }
+    for (; j < d; j += kG)
       if (probe_bits(bs, y, xs[j])) { credit(lc, t, xs, (int)j); ++c; }
-    return c;
-  }
-  const uint32_t lg = 32 - __clz(y.len);
-  if ((uint64_t)a * lg * 4 < y.len) {  // galloping side: A's elements binary-search N+(y)
+  } else if (kd == kStream) {
+    const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
+    for (uint32_t k = gl; k * 4 < y.len; k += kG) {
+      const uint4 v = __ldg(yl + k);
+      const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (k * 4 + q >= y.len) break;
+        const int j = X.index_of(e[q]);
+        if (j >= 0) { credit(lc, t, xs, j); ++c; }
+      }
+    }
+  } else if (kd == kSearch) {
     for (uint32_t j = i + 1 + gl; j < d; j += kG)
       if (gmem_search(col + (uint64_t)y.list * 4, y.len, xs[j])) { credit(lc, t, xs, (int)j); ++c; }
-    return c;
-  }
-  const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;  // stream N+(y)
-  for (uint32_t k = gl; k * 4 < y.len; k += kG) {
-    const uint4 v = __ldg(yl + k);
-    const uint32_t e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (k * 4 + q >= y.len) break;
-      const int j = H.lookup(e[q]);
-      if (j >= 0) { credit(lc, t, xs, j); ++c; }
-    }
   }
   return c;
 }
@@ -126,22 +197,27 @@ __device__ __forceinline__ uint32_t group_sum(uint32_t v, uint32_t lane) {
   return v;
 }
 
+// ------------------------------------------------------------ warp kernel --
 struct __align__(16) PvWarpSmem {
-  uint32_t xs[kPvWarpMaxD];
-  uint32_t lc[kPvWarpMaxD];
-  uint32_t keys[kPvWHash];
-  uint16_t idx[kPvWHash];
+  uint32_t xs[kWarpMaxD];
+  uint32_t lc[kWarpMaxD];
+  uint32_t tab[kWarpTabWords];
+  YInfo yi[kWarpMaxD];
+  uint16_t pos[kWarpTabWords];
+  uint8_t kind[kWarpMaxD];
+  uint8_t ord[kWarpMaxD];
 };
 
-__global__ void __launch_bounds__(kPvWarps * 32) k_pv_warp(const uint4* __restrict__ desc,
-                                                          const uint32_t* __restrict__ col,
-                                                          const uint32_t* __restrict__ bs,
-                                                          const uint32_t* __restrict__ work, uint64_t nwork,
-                                                          unsigned long long* __restrict__ t,
-                                                          unsigned long long* __restrict__ ctr) {
-  __shared__ PvWarpSmem sm_all[kPvWarps];
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, grp = lane / kG, gl = lane % kG;
-  PvWarpSmem& sm = sm_all[w];
+__global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict__ desc,
+                                                        const uint32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ bs,
+                                                        const uint32_t* __restrict__ work, uint64_t nwork,
+                                                        unsigned long long* __restrict__ t,
+                                                        unsigned long long* __restrict__ ctr) {
+  extern __shared__ __align__(16) uint32_t dsm_pw[];
+  PvWarpSmem& sm = reinterpret_cast<PvWarpSmem*>(dsm_pw)[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31, grp = lane / kG, gl = lane % kG;
+  const unsigned lt = (1u << lane) - 1u;
   for (;;) {
     unsigned long long wi = 0;
     if (lane == 0) wi = atomicAdd(&ctr[1], 1ull);
@@ -149,44 +225,70 @@ __global__ void __launch_bounds__(kPvWarps * 32) k_pv_warp(const uint4* __restri
     if (wi >= nwork) break;
     const uint32_t x = __ldg(work + wi);
     const uint4 dx = __ldg(desc + x);
-    const uint32_t d = dx.y;  // 2 <= d <= kPvWarpMaxD
+    const uint32_t d = dx.y;  // 2 <= d <= kWarpMaxD
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
     for (uint32_t k = lane; k < d; k += 32) sm.lc[k] = 0u;
     __syncwarp();
-    const IdxHash H = build_idx_hash<false>(sm.keys, sm.idx, sm.xs, d, true, lane, 32);
-    __syncwarp();
-    uint32_t cx = 0;
-    for (uint32_t i = grp; i + 1 < d; i += 32 / kG) {
+    const XIdx X = plan_x(sm.tab, sm.pos, kWarpTabWords, sm.xs, d);
+    const uint32_t nrows = d - 1;
+    bool need_x = false;  // only STREAM rows read x's staged structure
+    for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
-      const uint32_t c = group_sum(pv_row(y, sm.xs, d, i, H, sm.lc, t, col, bs, gl), lane);
-      if (gl == 0 && c) atomicAdd(&t[sm.xs[i]], (unsigned long long)c);
-      if (gl == 0) cx += c;
+      const uint8_t kd = row_kind(y, nrows - i, X);
+      sm.yi[i] = y;
+      sm.kind[i] = kd;
+      need_x |= kd == kStream;
+    }
+    if (__any_sync(kFull, need_x)) fill_x<false>(X, lane, 32);
+    __syncwarp();
+    uint32_t nr = 0;
+#pragma unroll
+    for (int kdi = 0; kdi < 3; ++kdi) {
+      const uint8_t want = (uint8_t)(kProbe + kdi);
+      for (uint32_t i0 = 0; i0 < nrows; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool sel = i < nrows && sm.kind[i] == want;
+        const unsigned m = __ballot_sync(kFull, sel);
+        if (sel) sm.ord[nr + __popc(m & lt)] = (uint8_t)i;
+        nr += __popc(m);
+      }
     }
     __syncwarp();
+    uint32_t cx = 0;
+    for (uint32_t r = grp; r < nr; r += 32 / kG) {
+      const uint32_t i = sm.ord[r];
+      const uint32_t c = group_sum(pv_row(sm.kind[i], sm.yi[i], X, i, sm.lc, t, col, bs, gl), lane);
+      if (gl == 0 && c) {
+        atomicAdd(&sm.lc[i], c);  // y = N+(x)[i] is in every triangle of its row
+        cx += c;
+      }
+    }
     cx = warp_sum(cx);
     if (lane == 0 && cx) atomicAdd(&t[x], (unsigned long long)cx);
+    __syncwarp();
     for (uint32_t k = lane; k < d; k += 32)
       if (sm.lc[k]) atomicAdd(&t[sm.xs[k]], (unsigned long long)sm.lc[k]);
     __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(kPvCtaWarps * 32) k_pv_cta(const uint4* __restrict__ desc,
-                                                            const uint32_t* __restrict__ col,
-                                                            const uint32_t* __restrict__ bs,
-                                                            const uint32_t* __restrict__ work, uint64_t nwork,
-                                                            unsigned long long* __restrict__ t,
-                                                            unsigned long long* __restrict__ ctr) {
-  extern __shared__ __align__(16) uint32_t dsm_pv[];
-  uint32_t* xs_s = dsm_pv;                  // kPvCtaXCap
-  uint32_t* lc_s = xs_s + kPvCtaXCap;       // kPvCtaXCap
-  uint32_t* keys = lc_s + kPvCtaXCap;       // kPvCHash
-  uint16_t* idx = reinterpret_cast<uint16_t*>(keys + kPvCHash);  // kPvCHash
+// ------------------------------------------------------------- CTA kernel --
+__global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restrict__ desc,
+                                                          const uint32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ bs,
+                                                          const uint32_t* __restrict__ work, uint64_t nwork,
+                                                          unsigned long long* __restrict__ t,
+                                                          unsigned long long* __restrict__ ctr, uint32_t xcap) {
+  extern __shared__ __align__(16) uint32_t dsm_pc[];
+  uint32_t* xs_s = dsm_pc;                                          // xcap
+  uint32_t* lc_s = xs_s + xcap;                                     // xcap
+  uint32_t* tab = lc_s + xcap;                                      // kCtaTabWords
+  uint16_t* pos = reinterpret_cast<uint16_t*>(tab + kCtaTabWords);  // kCtaTabWords
   __shared__ unsigned long long s_wi;
   __shared__ uint32_t s_cx;
-  constexpr uint32_t kGroups = kPvCtaWarps * 32 / kG;
+  constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
   const uint32_t lane = threadIdx.x & 31, gid = threadIdx.x / kG, gl = threadIdx.x % kG;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -200,23 +302,33 @@ __global__ void __launch_bounds__(kPvCtaWarps * 32) k_pv_cta(const uint4* __rest
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
-    const bool staged = d <= (uint32_t)kPvCtaXCap;
+    const bool staged = d <= xcap;
     const uint32_t* xs = staged ? xs_s : xg;
-    uint32_t* lc = staged ? lc_s : nullptr;  // d > kPvCtaXCap: credit z with global atomics
+    uint32_t* lc = staged ? lc_s : nullptr;  // d > xcap: credit with global atomics
     if (staged) {
       for (uint32_t k = threadIdx.x; k < (d + 3) / 4; k += blockDim.x)
         reinterpret_cast<uint4*>(xs_s)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
       for (uint32_t k = threadIdx.x; k < d; k += blockDim.x) lc_s[k] = 0u;
     }
     __syncthreads();
-    const IdxHash H = build_idx_hash<true>(keys, idx, xs, d, staged, threadIdx.x, blockDim.x);
+    const XIdx X = plan_x(tab, pos, staged ? kCtaTabWords : 0, xs, d);
+    fill_x<true>(X, threadIdx.x, blockDim.x);
     __syncthreads();
+    const uint32_t nrows = d - 1;
     uint32_t cx = 0;
-    for (uint32_t i = gid; i + 1 < d; i += kGroups) {
-      const YInfo y = yinfo(desc, xs[i]);
-      const uint32_t c = group_sum(pv_row(y, xs, d, i, H, lc, t, col, bs, gl), lane);
-      if (gl == 0 && c) atomicAdd(&t[xs[i]], (unsigned long long)c);
-      if (gl == 0) cx += c;
+    uint32_t i = gid;
+    YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
+    while (i < nrows) {
+      const uint32_t inext = i + kGroups;
+      const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
+      const uint32_t c = group_sum(pv_row(row_kind(y, nrows - i, X), y, X, i, lc, t, col, bs, gl), lane);
+      if (gl == 0 && c) {
+        if (lc) atomicAdd(&lc[i], c);
+        else atomicAdd(&t[xs[i]], (unsigned long long)c);
+        cx += c;
+      }
+      i = inext;
+      y = ynext;
     }
     cx = warp_sum(cx);
     if (lane == 0 && cx) atomicAdd(&s_cx, cx);
@@ -229,7 +341,7 @@ __global__ void __launch_bounds__(kPvCtaWarps * 32) k_pv_cta(const uint4* __rest
   }
 }
 
-constexpr size_t kPvCtaSmem = (size_t)(2 * kPvCtaXCap + kPvCHash) * 4 + (size_t)kPvCHash * 2;
+size_t cta_smem(uint32_t xcap) { return (size_t)(2 * xcap + kCtaTabWords) * 4 + (size_t)kCtaTabWords * 2; }
 
 // ---- 128-bit reductions for the root GHD node ----
 __device__ __forceinline__ void add_u128_atomic(unsigned long long* out2, unsigned long long lo,
@@ -289,15 +401,23 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];
   const uint64_t nlarge = g->n_work[2];
   if (nlarge) {
-    EH_CUDA(cudaFuncSetAttribute(k_pv_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPvCtaSmem));
-    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-    k_pv_cta<<<grid, kPvCtaWarps * 32, kPvCtaSmem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, d_t,
-                                                         g->d_counter);
+    uint32_t xcap = kCtaXCapMin;
+    while (xcap < g->max_dplus && xcap < kCtaXCapMax) xcap *= 2;
+    if (const char* e = getenv("EH_PV_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: forces the unstaged path
+    const size_t smem = cta_smem(xcap);
+    EH_CUDA(cudaFuncSetAttribute(k_pv_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pv_cta, kCtaWarps * 32, smem));
+    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, d_t,
+                                                 g->d_counter, xcap);
     EH_LAUNCH("k_pv_cta");
   }
   if (nsmall) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kPvWarps - 1) / kPvWarps, (uint64_t)kSMs * 8);
-    k_pv_warp<<<grid, kPvWarps * 32, 0, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, g->d_counter);
+    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWarps - 1) / kWarps, (uint64_t)kSMs * 8);
+    const size_t smem = sizeof(PvWarpSmem) * kWarps;
+    EH_CUDA(cudaFuncSetAttribute(k_pv_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pv_warp<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, g->d_counter);
     EH_LAUNCH("k_pv_warp");
   }
 }

@@ -55,7 +55,7 @@ def test_kn_closed_forms(n):
     assert bar == n * (n - 1) * (2 * tv) ** 2
 
 
-def test_k1700_barbell_above_2_64_and_unstaged_cta_path():
+def test_k1700_barbell_above_2_64():
     n = 1700
     _, t, lol, bar, _ = _gpu(*synth.complete(n))
     tv = comb(n - 1, 2)
@@ -65,7 +65,8 @@ def test_k1700_barbell_above_2_64_and_unstaged_cta_path():
 
 
 def test_multipartite_degree_above_stage_cap():
-    # K_{a,a,a}: all degrees 2a, so |N+(x)| runs up to 2a - 1 > 4096 (the unstaged CTA path); t(v) = a^2.
+    # K_{a,a,a}: all degrees 2a, so |N+(x)| runs up to 2a - 1 = 4199, above the CTA kernel's
+    # default staging capacity (2048; it grows to the next power of two); t(v) = a^2.
     a = 2100
     _, t, lol, bar, tri = _gpu(*synth.complete_multipartite((a, a, a)))
     assert tri == a**3 and np.all(t == a * a)
@@ -146,3 +147,14 @@ def test_config_vs_oracle(name, golden_dir):
     assert str(synth.checksum(src, dst)) == gold["checksum"]
     t, _, _ = _check(src, dst)
     assert int(t.sum()) == 3 * gold["triangles"]
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_unstaged_cta_path(seed, monkeypatch):
+    # EH_PV_XCAP (test hook) lowers the CTA kernel's staging capacity, so every
+    # |N+(x)| > 128 takes the unstaged path (global N+(x), global credit atomics).
+    monkeypatch.setenv("EH_PV_XCAP", "128")
+    _check(*synth.rmat(14, 16, 777 + seed))
+    a = 300
+    _, t, lol, bar, tri = _gpu(*synth.complete_multipartite((a, a, a)))
+    assert tri == a**3 and np.all(t == a * a)

@@ -17,7 +17,8 @@ import synth  # noqa: E402
 PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6538.6
-names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+NEXT1 = "--next1" in sys.argv
+names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"]
 reps = 5
 for name in names:
     cfg = synth.CONFIGS[name]
@@ -27,7 +28,7 @@ for name in names:
     d = torch.from_numpy(dst.view(np.int32)).cuda()
     del src, dst
     st = torch.cuda.Stream()
-    loads, tris, k4s = [], [], []
+    loads, tris, k4s, pvs, lols, bars = [], [], [], [], [], []
     res = {}
     for r in range(reps + 1):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -39,13 +40,29 @@ for name in names:
             e[2].record(st)
             k = g.count_4cliques() if cfg.query == "4cliques" else None
             e[3].record(st)
+            if NEXT1:  # t(v) into a device array, Lollipop, Barbell
+                e += [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                tv = torch.empty(g.stats().n_active if r == 0 else tv.numel(), dtype=torch.int64, device="cuda")
+                e[4].record(st)
+                g.triangles_per_vertex(tv)
+                e[5].record(st)
+                lol = g.count_lollipop()
+                e[6].record(st)
+                bar = g.count_barbell()
+                e[7].record(st)
             st.synchronize()
             if r == 0:
                 stats = g.stats()
             g.close()
         if r == 0:
             res.update(triangles=t, four_cliques=k)
+            if NEXT1:
+                res.update(lollipop=str(lol), barbell=str(bar), sum_t=int(tv.sum()))
             continue
+        if NEXT1:
+            pvs.append(e[4].elapsed_time(e[5]))
+            lols.append(e[5].elapsed_time(e[6]))
+            bars.append(e[6].elapsed_time(e[7]))
         loads.append(e[0].elapsed_time(e[1]))
         tris.append(e[1].elapsed_time(e[2]))
         if k is not None:
@@ -58,6 +75,11 @@ for name in names:
                step_edges_per_s=n_in / ((lt + tt) / 1e3), count_edges_per_s=n_in / (tt / 1e3))
     if k4s:
         res["k4_ms"] = statistics.median(k4s)
+    if pvs:
+        pv = statistics.median(pvs)
+        pv_bytes = stats.alg_bytes_tri + 8 * stats.n_active  # B_tri reads + the t(v) array
+        res.update(pv_ms=pv, lollipop_ms=statistics.median(lols), barbell_ms=statistics.median(bars),
+                   pv_alg_bytes=pv_bytes, pv_gbs=pv_bytes / pv / 1e6, pv_roofline_frac=pv_bytes / pv / 1e6 / PEAK)
     print(json.dumps(res), flush=True)
     del s, d
     torch.cuda.empty_cache()

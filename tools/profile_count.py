@@ -12,7 +12,7 @@ import paper_1503_02368_b200 as eh  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
-ap.add_argument("--query", default="tri", choices=["tri", "k4"])
+ap.add_argument("--query", default="tri", choices=["tri", "k4", "pv", "lollipop"])
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tau", type=int, default=0)
 ap.add_argument("--small", type=int, default=0)
@@ -23,6 +23,7 @@ with eh.Graph(src, dst, tau=a.tau, bin_small_max=a.small, bin_large_min=a.large)
     st = g.stats()
     for _ in range(a.reps):
         t0 = time.perf_counter()
-        c = g.count_triangles() if a.query == "tri" else g.count_4cliques()
+        c = {"tri": g.count_triangles, "k4": g.count_4cliques, "lollipop": g.count_lollipop,
+             "pv": lambda: int(g.triangles_per_vertex().sum())}[a.query]()
         print(f"{a.query} = {c}  {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
     print(st, flush=True)
