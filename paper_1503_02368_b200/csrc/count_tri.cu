@@ -26,7 +26,7 @@
 // group: 4 rows in flight per warp, and 8 lanes x 16 B still read one full
 // 128-B line per load.  Work classes (a7): 2 <= |N+(x)| <= kWarpMaxD run one
 // warp per x (rows ordered by kind so the 4 groups of a warp rarely diverge);
-// larger x run one CTA per x (64 groups over rows).  COUNT(*) is a per-lane
+// larger x run one 4-warp CTA per x (16 groups over rows).  COUNT(*) is a per-lane
 // u64, reduced with __shfl_xor_sync, one atomicAdd(unsigned long long) per warp
 // (PAPER.md:243).
 #include "eh_internal.cuh"
@@ -43,9 +43,10 @@ constexpr int kG = 8;                 // lanes per row group
 constexpr int kWarpMaxD = 128;        // warp kernel handles 2 <= d <= kWarpMaxD
 constexpr int kWarpBmWords = 512;     // warp-kernel x structure: 2 KB (bitmap of 16384 ids or 512-slot hash)
 constexpr int kWK_Warps = 8;
-constexpr int kCtaWarps = 16;
-constexpr int kCtaXCap = 4096;        // CTA kernel stages N+(x) in smem up to this size
-constexpr int kCtaBmWords = 16384;    // CTA-kernel x structure: 64 KB (bitmap of 524288 ids or hash)
+constexpr int kCtaWarps = 4;         // small CTAs (many per SM) balance the per-x tails best (measured)
+constexpr uint32_t kCtaXCapMax = 16384;  // CTA kernel stages N+(x) in smem up to xcap = max |N+(x)|
+                                         // rounded up to 256, clamped to this
+constexpr int kCtaBmWords = 2048;     // CTA-kernel x structure: 8 KB (bitmap of 65536 ids or hash)
 constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor * |A| + 8
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -55,7 +56,7 @@ enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2 };
 // ---------------------------------------------- x's membership structure --
 // N+(x) in shared memory as (a) an exact bitmap over [lo, lo + nbits), (b) an
 // open-addressing hash table with 2^hbits slots (load <= 1/4), or (c) the
-// sorted list itself (binary search; CTA kernel only when |N+(x)| > kCtaXCap).
+// sorted list itself (binary search; CTA kernel only when |N+(x)| > xcap).
 struct XSet {
   uint32_t* tab;        // bitmap words or hash slots (shared memory)
   const uint32_t* xs;   // sorted N+(x) (shared or global)
@@ -278,17 +279,17 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
 }
 
 // ------------------------------------------------------------- CTA kernel --
-// One CTA per x with |N+(x)| > kWarpMaxD; its 64 groups take rows round-robin
+// One CTA per x with |N+(x)| > kWarpMaxD; its 16 groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
 __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
                                                             const uint32_t* __restrict__ work, uint64_t nwork,
-                                                            unsigned long long* __restrict__ ctr) {
+                                                            unsigned long long* __restrict__ ctr, uint32_t xcap) {
   extern __shared__ __align__(16) uint32_t dsm[];
-  uint32_t* xs_s = dsm;             // kCtaXCap
-  uint32_t* tab = dsm + kCtaXCap;   // kCtaBmWords
+  uint32_t* xs_s = dsm;             // xcap
+  uint32_t* tab = dsm + xcap;       // kCtaBmWords
   __shared__ unsigned long long s_wi;
   constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
   const int lane = threadIdx.x & 31;
@@ -304,13 +305,13 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
     const uint32_t d = dx.y;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     const uint32_t* xs = xg;
-    if (d <= (uint32_t)kCtaXCap) {
+    if (d <= xcap) {
       for (uint32_t k = threadIdx.x; k < (d + 3) / 4; k += blockDim.x)
         reinterpret_cast<uint4*>(xs_s)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
       xs = xs_s;
     }
     __syncthreads();
-    const XSet X = build_xset(tab, (d <= (uint32_t)kCtaXCap) ? kCtaBmWords : 0, xs, d, threadIdx.x, blockDim.x);
+    const XSet X = build_xset(tab, (d <= xcap) ? kCtaBmWords : 0, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
     const uint32_t nrows = d - 1;
     uint32_t i = gid;
@@ -329,7 +330,6 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
-constexpr size_t kCtaSmem = (size_t)(kCtaXCap + kCtaBmWords) * 4;
 
 }  // namespace
 
@@ -340,9 +340,15 @@ uint64_t count_triangles(eh_graph* g) {
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];
   const uint64_t nlarge = g->n_work[2];
   if (nlarge) {
-    EH_CUDA(cudaFuncSetAttribute(k_tri_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmem));
-    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * 2);
-    k_tri_cta<<<grid, kCtaWarps * 32, kCtaSmem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter);
+    uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
+    if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
+    const size_t smem = (size_t)(xcap + kCtaBmWords) * 4;
+    EH_CUDA(cudaFuncSetAttribute(k_tri_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_cta, kCtaWarps * 32, smem));
+    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+    k_tri_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter,
+                                                 xcap);
     EH_LAUNCH("k_tri_cta");
   }
   if (nsmall) {

@@ -127,6 +127,16 @@ def test_ids_near_u32_max_dictionary_path():
     assert _check(s, d) == _check(src, dst)
 
 
+@pytest.mark.parametrize("seed", range(2))
+def test_unstaged_cta_path(seed, monkeypatch):
+    # EH_TRI_XCAP (test hook) lowers the triangle CTA kernel's staging capacity:
+    # every |N+(x)| > 128 then reads N+(x) from global memory (sorted-list mode).
+    monkeypatch.setenv("EH_TRI_XCAP", "128")
+    _check(*synth.rmat(14, 16, 555 + seed), k4=False)
+    a = 300
+    assert _gpu_counts(*synth.complete_multipartite((a, a, a)), k4=False)[0] == a**3
+
+
 def test_huge_star_and_hub():
     s, d = synth.star(200_000)
     assert _gpu_counts(s, d)[:2] == (0, 0)
