@@ -9,7 +9,9 @@
  *   4Clique(x,y,z,w) :- R(x,y),S(y,z),T(x,z),U(x,w),V(y,w),Q(z,w). PAPER.md:217
  *
  * with R = S = ... = the symmetrically pruned Edge relation
- * and COUNT(*) aggregated as `w:long`.  Everything below this
+ * and COUNT(*) aggregated as `w:long`, plus (SURVEY.md §8(f)
+ * NEXT-1) per-vertex triangle counts and the Lollipop / Barbell COUNT(*) by the
+ * two-phase GHD plan.  Everything below this
  * header runs on one GPU as hand-written CUDA kernels; there is no CPU
  * fallback: every entry point fails (returns an error) when no CUDA device is
  * usable.
@@ -65,9 +67,14 @@ typedef struct {
   void (*dev_free)(void* ptr, void* stream, void* ctx);
   void* alloc_ctx;
   uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT */
-  uint32_t bin_small_max;  /* count-kernel work classes; 0 -> tuned defaults. */
-  uint32_t bin_large_min;  /* bin_small_max = UINT32_MAX forces every vertex into the smallest class,
-                              bin_large_min = 1 forces every vertex into the largest class. */
+  /* Count-kernel work classes by d = |N+(x)|: 0 = [2, bin_small_max], 1 = up to
+   * bin_large_min - 1, 2 = the rest.  Triangle / per-vertex kernels: class 0 warp-per-x,
+   * classes 1-2 CTA-per-x; 4-clique kernels: classes 0-1 warp-per-x, class 2 CTA-per-x.
+   * 0 -> tuned defaults (64, 129).  Both are clamped to the warp
+   * kernels' capacity (d <= 128): bin_small_max = UINT32_MAX puts every d <= 128 into
+   * class 0, bin_large_min = 1 puts every vertex into class 2.  Counts do not depend on them. */
+  uint32_t bin_small_max;
+  uint32_t bin_large_min;
   uint32_t min_bitset_card;/* bitset only if |S| >= this (reading c15); 0 -> 2 */
 } eh_config;
 

@@ -398,8 +398,8 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
   const uint64_t n = g->n_act;
   EH_CUDA(cudaMemsetAsync(d_t, 0, std::max<uint64_t>(1, n) * 8, s));
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
-  const uint64_t nsmall = g->n_work[0] + g->n_work[1];
-  const uint64_t nlarge = g->n_work[2];
+  const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
+  const uint64_t nlarge = g->n_work[1] + g->n_work[2];
   if (nlarge) {
     uint32_t xcap = kCtaXCapMin;
     while (xcap < g->max_dplus && xcap < kCtaXCapMax) xcap *= 2;

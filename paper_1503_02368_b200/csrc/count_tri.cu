@@ -336,9 +336,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
 uint64_t count_triangles(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
-  // work classes 0 and 1 (d <= kWarpMaxD) -> warp kernel; class 2 -> CTA kernel
-  const uint64_t nsmall = g->n_work[0] + g->n_work[1];
-  const uint64_t nlarge = g->n_work[2];
+  const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
+  const uint64_t nlarge = g->n_work[1] + g->n_work[2];
   if (nlarge) {
     uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path

@@ -163,23 +163,24 @@ void compute_stats(eh_graph* g) {
 }
 
 void build_worklists(eh_graph* g) {
-  // class(d) = 0 if d <= small_max; else 2 if d >= large_min; else 1 (d >= 2 only).
+  // Three classes by d = |N+(x)| (d >= 2 only): 0 = [2, small_max], 1 = (small_max, large_min),
+  // 2 = [large_min, inf).  The triangle and per-vertex kernels run class 0 warp-per-x and
+  // classes 1-2 CTA-per-x; the 4-clique kernels run classes 0-1 warp-per-x and class 2
+  // CTA-per-x.  The warp kernels stage N+(x) in a fixed shared-memory slot, so d above
+  // their capacity always lands in class 2 whatever the configuration asks for.
   Allocator& al = g->alloc;
   cudaStream_t s = g->stream;
   const uint64_t n = g->n_act;
-  // classes 0/1 run the warp-per-x kernels, class 2 the CTA-per-x kernels; the
-  // warp kernels stage N+(x) in a fixed shared-memory slot, so d above their
-  // capacity always lands in class 2 whatever the configuration asks for.
   const uint64_t cap = (uint64_t)tri_warp_max_degree() + 1;
-  const uint64_t small_max = g->bin_small_max ? g->bin_small_max : 32;
   const uint64_t large_min = std::min<uint64_t>(g->bin_large_min ? g->bin_large_min : cap, cap);
+  const uint64_t small_max = std::min<uint64_t>(g->bin_small_max ? g->bin_small_max : 64, large_min - 1);
   g->work = (uint32_t*)g->own(std::max<uint64_t>(1, n) * 4);
   uint64_t lo[3], hi[3];  // class c holds lo[c] <= d < hi[c]
   lo[0] = 2;
   hi[0] = std::max<uint64_t>(2, small_max + 1);
   lo[1] = hi[0];
   hi[1] = std::max<uint64_t>(lo[1], large_min);
-  lo[2] = std::max<uint64_t>(hi[1], 2);
+  lo[2] = hi[1];
   hi[2] = 1ull << 33;
   uint64_t pos = 0;
   for (int c = 0; c < 3; ++c) {
