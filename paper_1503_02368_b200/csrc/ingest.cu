@@ -163,27 +163,51 @@ __global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint
 }
 
 // a5: orient low rank -> high rank: out-degree histogram of the low end.
+// Keys arrive sorted by their low id, so runs of equal low ends are common
+// inside a warp: atomics are aggregated over equal targets (__match_any_sync).
 __global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint32_t* __restrict__ rank,
                          uint32_t* __restrict__ dplus) {
   const uint64_t mask = (1ull << b) - 1ull;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    const uint32_t ru = rank[k >> b], rv = rank[k & mask];
-    atomicAdd(&dplus[min(ru, rv)], 1u);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
+    const uint64_t i = base + lane;
+    uint32_t lo = 0xFFFFFFFFu;
+    if (i < m) {
+      const uint64_t k = keys[i];
+      lo = min(rank[k >> b], rank[k & mask]);
+    }
+    const unsigned peers = __match_any_sync(kFull, lo);
+    if (lo != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&dplus[lo], (uint32_t)__popc(peers));
   }
 }
 
 // a5: counting-sort scatter of the high end into the low end's padded list
-// (slot order within a list is arbitrary; segmented_sort_u32 orders it).
+// (slot order within a list is arbitrary; segmented_sort_u32 orders it).  One
+// cursor atomic per group of equal low ends in the warp.
 __global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b,
                               const uint32_t* __restrict__ rank, const uint64_t* __restrict__ off16,
                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ col) {
   const uint64_t mask = (1ull << b) - 1ull;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    const uint32_t ru = rank[k >> b], rv = rank[k & mask];
-    const uint32_t lo = min(ru, rv), hi = max(ru, rv);
-    col[off16[lo] * 4 + atomicAdd(&cursor[lo], 1u)] = hi;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
+    const uint64_t i = base + lane;
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    if (i < m) {
+      const uint64_t k = keys[i];
+      const uint32_t ru = rank[k >> b], rv = rank[k & mask];
+      lo = min(ru, rv);
+      hi = max(ru, rv);
+    }
+    const unsigned peers = __match_any_sync(kFull, lo);
+    const int leader = __ffs(peers) - 1;
+    uint32_t p0 = 0;
+    if (lo != 0xFFFFFFFFu && lane == leader) p0 = atomicAdd(&cursor[lo], (uint32_t)__popc(peers));
+    p0 = __shfl_sync(peers, p0, leader);
+    if (lo != 0xFFFFFFFFu) col[off16[lo] * 4 + p0 + __popc(peers & lt)] = hi;
   }
 }
 
