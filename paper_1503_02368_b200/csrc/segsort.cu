@@ -5,8 +5,9 @@
 // cursor per list), which leaves each list in arbitrary order.  Degree
 // orientation bounds every list: |N+(x)| <= sqrt(2m) (each out-neighbour has
 // degree >= deg(x) >= |N+(x)|), so lists are short and sort in on-chip memory:
-//   len <= 32          one warp, bitonic network in registers (__shfl_xor_sync)
-//   33 .. 1024         one warp, bitonic network in shared memory
+//   len <= 256         one warp, bitonic network in registers, E = 1, 2, 4 or 8
+//                      keys per lane (__shfl_xor_sync across lanes)
+//   257 .. 1024        one warp, bitonic network in shared memory
 //   1025 .. 8192       one CTA, bitonic network in shared memory
 //   longer (rare)      gathered as (segment << 32 | value) keys and sorted by the
 //                      device-wide LSD radix sort, then scattered back.
@@ -28,7 +29,39 @@ struct Seg {
   const uint32_t* len;
 };
 
-__global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
+// Bitonic network over 32 * E keys held E per lane (key index e * 32 + lane, so
+// loads and stores are coalesced).
+template <int E>
+__device__ __forceinline__ void warp_bitonic_regs(uint32_t (&x)[E], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {  // partner in this lane: e ^ (j / 32)
+        const int je = j >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & je) continue;
+          const bool up = (((e * 32 + lane) & k) == 0);
+          const uint32_t a = x[e], b = x[e + je];
+          x[e] = up ? min(a, b) : max(a, b);
+          x[e + je] = up ? max(a, b) : min(a, b);
+        }
+      } else {  // partner in lane ^ j
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t o = __shfl_xor_sync(kFull, x[e], j);
+          const bool up = (((e * 32 + lane) & k) == 0);
+          x[e] = (lower == up) ? min(x[e], o) : max(x[e], o);
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -36,17 +69,18 @@ __global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t*
     const uint32_t v = ids[t];
     const uint32_t n = sg.len[v];
     uint32_t* p = data + sg.off16[v] * 4;
-    uint32_t x = (lane < (int)n) ? p[lane] : kPad;
+    uint32_t x[E];
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const uint32_t o = __shfl_xor_sync(kFull, x, j);
-        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-        x = (lower == up) ? min(x, o) : max(x, o);
-      }
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = e * 32 + lane;
+      x[e] = (i < n) ? p[i] : kPad;
     }
-    if (lane < (int)n) p[lane] = x;
+    warp_bitonic_regs<E>(x, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = e * 32 + lane;
+      if (i < n) p[i] = x[e];
+    }
   }
 }
 
@@ -147,19 +181,23 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
   if (nseg == 0 || max_len <= 1) return;
   const Seg sg{off16, len};
   DBuf<uint32_t> ids(al, nseg);
-  const uint32_t bounds[4][2] = {{2, 32}, {33, (uint32_t)kMidMax}, {(uint32_t)kMidMax + 1, (uint32_t)kBigMax},
-                                 {(uint32_t)kBigMax + 1, 0xFFFFFFFFu}};
-  for (int tier = 0; tier < 4; ++tier) {
+  const uint32_t bounds[7][2] = {{2, 32}, {33, 64}, {65, 128}, {129, 256}, {257, (uint32_t)kMidMax},
+                                 {(uint32_t)kMidMax + 1, (uint32_t)kBigMax}, {(uint32_t)kBigMax + 1, 0xFFFFFFFFu}};
+  for (int tier = 0; tier < 7; ++tier) {
     if (max_len < bounds[tier][0]) break;
     const uint64_t k = select_if(nseg, LenPred{len, bounds[tier][0], bounds[tier][1]}, IdEmit{ids.p}, al, s);
     if (k == 0) continue;
-    if (tier == 0) {
-      k_seg_small<<<grid_for(k * 32, 256), 256, 0, s>>>(data, sg, ids.p, k);
-      EH_LAUNCH("k_seg_small");
-    } else if (tier == 1) {
+    if (tier <= 3) {
+      const unsigned g = grid_for(k * 32, 256);
+      if (tier == 0) k_seg_regs<1><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      EH_LAUNCH("k_seg_regs");
+    } else if (tier == 4) {
       k_seg_mid<<<grid_for(k, kMidWarps), kMidWarps * 32, 0, s>>>(data, sg, ids.p, k);
       EH_LAUNCH("k_seg_mid");
-    } else if (tier == 2) {
+    } else if (tier == 5) {
       k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, ids.p, k);
       EH_LAUNCH("k_seg_big");
     } else {
