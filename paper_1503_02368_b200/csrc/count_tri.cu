@@ -26,7 +26,7 @@
 // group: 4 rows in flight per warp, and 8 lanes x 16 B still read one full
 // 128-B line per load.  Work classes (a7): 2 <= |N+(x)| <= kWarpMaxD run one
 // warp per x (rows ordered by kind so the 4 groups of a warp rarely diverge);
-// larger x run one 4-warp CTA per x (16 groups over rows).  COUNT(*) is a per-lane
+// larger x run one CTA per x (its groups take rows round-robin).  COUNT(*) is a per-lane
 // u64, reduced with __shfl_xor_sync, one atomicAdd(unsigned long long) per warp
 // (PAPER.md:243).
 #include "eh_internal.cuh"
@@ -43,10 +43,13 @@ constexpr int kG = 8;                 // lanes per row group
 constexpr int kWarpMaxD = 128;        // warp kernel handles 2 <= d <= kWarpMaxD
 constexpr int kWarpBmWords = 512;     // warp-kernel x structure: 2 KB (bitmap of 16384 ids or 512-slot hash)
 constexpr int kWK_Warps = 8;
-constexpr int kCtaWarps = 4;         // small CTAs (many per SM) balance the per-x tails best (measured)
+// CTA kernel shapes (measured on C2-C5): small CTAs with an 8 KB x
+// structure (bitmap of 65536 ids), many per SM, balance the per-x tails best --
+// unless the id space is so large that the spans of N+(x) outgrow that bitmap
+// (C5: 2^26 ids), where 16-warp CTAs with a 64 KB structure win.
 constexpr uint32_t kCtaXCapMax = 16384;  // CTA kernel stages N+(x) in smem up to xcap = max |N+(x)|
                                          // rounded up to 256, clamped to this
-constexpr int kCtaBmWords = 2048;     // CTA-kernel x structure: 8 KB (bitmap of 65536 ids or hash)
+constexpr uint64_t kWideIds = 1ull << 24;  // n_active above this -> the wide shape
 constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor * |A| + 8
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -279,17 +282,19 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
 }
 
 // ------------------------------------------------------------- CTA kernel --
-// One CTA per x with |N+(x)| > kWarpMaxD; its 16 groups take rows round-robin
+// One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
+template <int kCtaWarps, int kTabW, int kXCap>  // kXCap > 0: compile-time staging capacity, else xcap_rt
 __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
                                                             const uint32_t* __restrict__ work, uint64_t nwork,
-                                                            unsigned long long* __restrict__ ctr, uint32_t xcap) {
+                                                            unsigned long long* __restrict__ ctr, uint32_t xcap_rt) {
+  const uint32_t xcap = kXCap > 0 ? (uint32_t)kXCap : xcap_rt;
   extern __shared__ __align__(16) uint32_t dsm[];
   uint32_t* xs_s = dsm;             // xcap
-  uint32_t* tab = dsm + xcap;       // kCtaBmWords
+  uint32_t* tab = dsm + xcap;       // kTabW
   __shared__ unsigned long long s_wi;
   constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
   const int lane = threadIdx.x & 31;
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
       xs = xs_s;
     }
     __syncthreads();
-    const XSet X = build_xset(tab, (d <= xcap) ? kCtaBmWords : 0, xs, d, threadIdx.x, blockDim.x);
+    const XSet X = build_xset(tab, (d <= xcap) ? (uint32_t)kTabW : 0u, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
     const uint32_t nrows = d - 1;
     uint32_t i = gid;
@@ -331,24 +336,34 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
 }
 
 
+template <int NW, int TABW, int XCAP>
+void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
+  if (XCAP > 0) xcap = XCAP;
+  auto k = k_tri_cta<NW, TABW, XCAP>;
+  const size_t smem = (size_t)(xcap + TABW) * 4;
+  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, smem));
+  const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+  k<<<grid, NW * 32, smem, g->stream>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter, xcap);
+  EH_LAUNCH("k_tri_cta");
+}
+
 }  // namespace
 
 uint64_t count_triangles(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
-  const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
-  const uint64_t nlarge = g->n_work[1] + g->n_work[2];
+  // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
+  const bool wide = g->n_act > kWideIds;
+  const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
+  const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
   if (nlarge) {
     uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
-    const size_t smem = (size_t)(xcap + kCtaBmWords) * 4;
-    EH_CUDA(cudaFuncSetAttribute(k_tri_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_cta, kCtaWarps * 32, smem));
-    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-    k_tri_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter,
-                                                 xcap);
-    EH_LAUNCH("k_tri_cta");
+    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096>(g, nsmall, nlarge, 0);
+    else if (wide) launch_cta<16, 16384, 0>(g, nsmall, nlarge, xcap);
+    else launch_cta<4, 2048, 0>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps, (uint64_t)kSMs * 8);
