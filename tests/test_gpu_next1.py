@@ -158,3 +158,21 @@ def test_unstaged_cta_path(seed, monkeypatch):
     a = 300
     _, t, lol, bar, tri = _gpu(*synth.complete_multipartite((a, a, a)))
     assert tri == a**3 and np.all(t == a * a)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_config_vs_oracle_next1_golden(name, golden_dir):
+    """Full-size configs against the oracle's stored NEXT-1 values
+    (tools/write_oracle_goldens.py --next1): Lollipop, Barbell and the sha256 of
+    t(v) in ascending original-id order."""
+    import hashlib
+    gold = json.load(open(os.path.join(golden_dir, "configs_oracle.json")))["configs"].get(name, {})
+    if "next1" not in gold:
+        pytest.skip(f"no stored NEXT-1 oracle values for {name}")
+    src, dst = synth.CONFIGS[name].generate()
+    assert str(synth.checksum(src, dst)) == gold["checksum"]
+    ids, t, lol, bar, tri = _gpu(src, dst)
+    assert tri == gold["triangles"]
+    assert int(t.sum()) == gold["next1"]["sum_t"] == 3 * tri
+    assert hashlib.sha256(t.astype("<u8").tobytes()).hexdigest() == gold["next1"]["t_sha256"]
+    assert lol == int(gold["next1"]["lollipop"]) and bar == int(gold["next1"]["barbell"])

@@ -5,8 +5,11 @@ Calls only synth/ (inputs) and oracle/ (counts) -- never the CUDA path -- so the
 stored values are oracle values (task rule: "a stored value is ... written by a
 committed script that calls only oracle/").  Usage:
     python tools/write_oracle_goldens.py C1 C2 C3 C4 C5
-Existing entries for other configs are kept.
+Existing entries for other configs are kept.  With --next1, also the NEXT-1
+values: Lollipop / Barbell COUNT(*) and the sha256 of the
+per-vertex triangle counts t(v) (uint64, in ascending original-id order).
 """
+import hashlib
 import json
 import os
 import sys
@@ -20,7 +23,7 @@ import synth  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "configs_oracle.json")
 
 
-def main(names):
+def main(names, next1=False):
     data = json.load(open(OUT)) if os.path.exists(OUT) else {
         "citation": "BASELINE.json configs (SURVEY.md §8 C1..C5); values computed by oracle/eh_oracle.c "
                     "via tools/write_oracle_goldens.py on synthetic inputs from synth/ (DESIGN.md §4)",
@@ -44,11 +47,21 @@ def main(names):
         entry["oracle_seconds"] = {"generate": round(t1 - t0, 1), "ingest": round(t2 - t1, 1),
                                    "triangles": round(t3 - t2, 1), "four_cliques": round(t4 - t3, 1),
                                    "threads": oracle.default_threads()}
+        if next1:
+            tv = g.triangles_per_vertex()
+            entry["next1"] = {"sum_t": int(tv.sum(dtype="uint64")),
+                              "t_sha256": hashlib.sha256(tv.astype("<u8").tobytes()).hexdigest(),
+                              "lollipop": str(g.count_lollipop()), "barbell": str(g.count_barbell()),
+                              "seconds": round(time.time() - t4, 1)}
         g.close()
+        old = data["configs"].get(name, {})
+        if not next1 and "next1" in old:
+            entry["next1"] = old["next1"]
         data["configs"][name] = entry
         json.dump(data, open(OUT, "w"), indent=1)
         print(name, entry, flush=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["C1", "C2", "C3", "C4"])
+    args = [a for a in sys.argv[1:] if a != "--next1"]
+    main(args or ["C1", "C2", "C3", "C4"], next1="--next1" in sys.argv)
