@@ -47,6 +47,10 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
             f.restype = ctypes.c_uint64
+        for name in ("oracle_count_triangles_unpruned", "oracle_count_4cliques_unpruned"):
+            f = getattr(lib, name)
+            f.argtypes = [vp, ctypes.c_int]
+            f.restype = ctypes.c_uint64
         lib.oracle_triangles_at.argtypes = [vp, ctypes.c_uint32]
         lib.oracle_triangles_at.restype = ctypes.c_uint64
         lib.oracle_intersect.argtypes = [u32p, ctypes.c_uint64, u32p, ctypes.c_uint64, u32p]
@@ -113,6 +117,20 @@ class Graph:
 
     def count_4cliques_range(self, x0: int, x1: int, threads: int | None = None) -> int:
         return int(_load().oracle_count_4cliques_range(self._h, x0, x1, threads or default_threads()))
+
+    def count_triangles_unpruned(self, threads: int | None = None) -> int:
+        """NEXT-2: the triangle Generic-Join on the symmetric (unpruned) data = 6T."""
+        r = int(_load().oracle_count_triangles_unpruned(self._h, threads or default_threads()))
+        if r == 2**64 - 1:
+            raise MemoryError("oracle allocation failed")
+        return r
+
+    def count_4cliques_unpruned(self, threads: int | None = None) -> int:
+        """NEXT-2: the 4-clique Generic-Join on the symmetric (unpruned) data = 24 K4."""
+        r = int(_load().oracle_count_4cliques_unpruned(self._h, threads or default_threads()))
+        if r == 2**64 - 1:
+            raise MemoryError("oracle allocation failed")
+        return r
 
     def triangles_at(self, x: int) -> int:
         return int(_load().oracle_triangles_at(self._h, x))

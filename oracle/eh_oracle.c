@@ -33,6 +33,8 @@
  *            for z in P cap pi_Z Q
  *              K += | P cap Q[z] |          (two scalar merges in total)
  *   COUNT(*) is a uint64 sum ("w:long"; reading c9).
+ *   NEXT-1 / NEXT-2: per-vertex counts + Lollipop / Barbell,
+ *   and the unpruned nests on the symmetric data -- see their sections below.
  *   intersect (Table `lst:eh_operators`): sorted merge.
  *
  * Parallelism: only the outermost x loop is split over pthreads, with one
@@ -59,6 +61,8 @@ typedef struct {
   uint32_t* deg;     /* [nv] degree */
   uint64_t* off;     /* [nv+1] out-list offsets */
   uint32_t* adj;     /* [m] out-neighbours (original ids), sorted per list */
+  uint64_t* soff;    /* NEXT-2, built on first use: [nv+1] offsets of the full neighbour lists */
+  uint32_t* sadj;    /* [2m] all neighbours (original ids), sorted per list */
 } oracle_graph;
 
 static int cmp_u64(const void* a, const void* b) {
@@ -84,7 +88,7 @@ static int precedes(const oracle_graph* g, uint64_t iu, uint64_t iv) {
 
 void oracle_free(oracle_graph* g) {
   if (!g) return;
-  free(g->vid); free(g->deg); free(g->off); free(g->adj); free(g);
+  free(g->vid); free(g->deg); free(g->off); free(g->adj); free(g->soff); free(g->sadj); free(g);
 }
 
 oracle_graph* oracle_build(const uint32_t* src, const uint32_t* dst, uint64_t n) {
@@ -214,12 +218,69 @@ static uint64_t k4_range(const oracle_graph* g, uint64_t x0, uint64_t x1, uint32
   return k;
 }
 
+/*
+ * NEXT-2: the same Generic-Join on the UNPRUNED data -- the
+ * symmetric Edge relation, every undirected edge in both directions, no
+ * symmetry breaking ("Default" vs "Symmetrically
+ * Filtered").  Every binding is an ordered tuple, so the results are 6T and
+ * 24 K4 ("a multiple of the former").
+ *   triangle: for x, for y in N(x): Q += |N(y) cap N(x)|
+ *   4-clique: for x, for y in N(x): P = N(y) cap N(x); for z in P: K += |P cap N(z)|
+ */
+#define NB(g, i) ((g)->sadj + (g)->soff[i])
+#define DN(g, i) ((g)->soff[(i) + 1] - (g)->soff[i])
+
+/* Full neighbour lists N(v) (sorted by original id) from E+; idempotent. */
+static int build_symmetric(oracle_graph* g) {
+  if (g->soff) return 0;
+  uint64_t* soff = (uint64_t*)calloc(g->nv + 1, sizeof(uint64_t));
+  uint32_t* sadj = (uint32_t*)malloc((2 * g->m ? 2 * g->m : 1) * sizeof(uint32_t));
+  uint64_t* fill = (uint64_t*)calloc(g->nv + 1, sizeof(uint64_t));
+  if (!soff || !sadj || !fill) { free(soff); free(sadj); free(fill); return -1; }
+  for (uint64_t i = 0; i < g->nv; ++i) soff[i + 1] = soff[i] + g->deg[i];
+  for (uint64_t x = 0; x < g->nv; ++x)
+    for (uint64_t e = g->off[x]; e < g->off[x + 1]; ++e) {
+      const uint64_t y = vindex(g, g->adj[e]);
+      sadj[soff[x] + fill[x]++] = g->adj[e];
+      sadj[soff[y] + fill[y]++] = g->vid[x];
+    }
+  for (uint64_t i = 0; i < g->nv; ++i) qsort(sadj + soff[i], soff[i + 1] - soff[i], sizeof(uint32_t), cmp_u32);
+  free(fill);
+  g->sadj = sadj;
+  g->soff = soff;
+  return 0;
+}
+
+static uint64_t tri_unpruned_range(const oracle_graph* g, uint64_t x0, uint64_t x1) {
+  uint64_t q = 0;
+  for (uint64_t x = x0; x < x1; ++x)
+    for (uint64_t e = g->soff[x]; e < g->soff[x + 1]; ++e) {
+      const uint64_t y = vindex(g, g->sadj[e]);
+      q += merge_count(NB(g, y), DN(g, y), NB(g, x), DN(g, x));
+    }
+  return q;
+}
+
+static uint64_t k4_unpruned_range(const oracle_graph* g, uint64_t x0, uint64_t x1, uint32_t* P) {
+  uint64_t k = 0;
+  for (uint64_t x = x0; x < x1; ++x)
+    for (uint64_t e = g->soff[x]; e < g->soff[x + 1]; ++e) {
+      const uint64_t y = vindex(g, g->sadj[e]);
+      const uint64_t np = merge_into(NB(g, y), DN(g, y), NB(g, x), DN(g, x), P);
+      for (uint64_t t = 0; t < np; ++t) {
+        const uint64_t z = vindex(g, P[t]);
+        k += merge_count(P, np, NB(g, z), DN(g, z));
+      }
+    }
+  return k;
+}
+
 typedef struct {
   const oracle_graph* g;
   uint64_t x0, x1;
   volatile uint64_t* next;
   pthread_mutex_t* mu;
-  int query; /* 0 = triangles, 1 = 4-cliques */
+  int query; /* 0 = triangles, 1 = 4-cliques, 2 / 3 = the same, unpruned (NEXT-2) */
   uint64_t sum;
   int err;
 } job_t;
@@ -227,8 +288,11 @@ typedef struct {
 static void* worker(void* arg) {
   job_t* j = (job_t*)arg;
   uint32_t* P = NULL;
-  if (j->query == 1) {
-    P = (uint32_t*)malloc((j->g->max_out ? j->g->max_out : 1) * sizeof(uint32_t));
+  if (j->query == 1 || j->query == 3) {
+    uint64_t cap = j->g->max_out;
+    if (j->query == 3)
+      for (uint64_t i = 0; i < j->g->nv; ++i) cap = cap > j->g->deg[i] ? cap : j->g->deg[i];
+    P = (uint32_t*)malloc((cap ? cap : 1) * sizeof(uint32_t));
     if (!P) { j->err = 1; return NULL; }
   }
   const uint64_t chunk = 64;
@@ -239,7 +303,10 @@ static void* worker(void* arg) {
     pthread_mutex_unlock(j->mu);
     if (a >= j->x1) break;
     const uint64_t b = (a + chunk < j->x1) ? a + chunk : j->x1;
-    j->sum += j->query == 0 ? tri_range(j->g, a, b) : k4_range(j->g, a, b, P);
+    j->sum += j->query == 0 ? tri_range(j->g, a, b)
+            : j->query == 1 ? k4_range(j->g, a, b, P)
+            : j->query == 2 ? tri_unpruned_range(j->g, a, b)
+                            : k4_unpruned_range(j->g, a, b, P);
   }
   free(P);
   return NULL;
@@ -270,6 +337,15 @@ static uint64_t run(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads
 }
 
 uint64_t oracle_count_triangles(const oracle_graph* g, int threads) { return run(g, 0, UINT64_MAX, threads, 0); }
+/* NEXT-2: unpruned (ordered-binding) counts on the symmetric data; UINT64_MAX on allocation failure. */
+uint64_t oracle_count_triangles_unpruned(oracle_graph* g, int threads) {
+  if (!g || build_symmetric(g)) return UINT64_MAX;
+  return run(g, 0, UINT64_MAX, threads, 2);
+}
+uint64_t oracle_count_4cliques_unpruned(oracle_graph* g, int threads) {
+  if (!g || build_symmetric(g)) return UINT64_MAX;
+  return run(g, 0, UINT64_MAX, threads, 3);
+}
 uint64_t oracle_count_4cliques(const oracle_graph* g, int threads) { return run(g, 0, UINT64_MAX, threads, 1); }
 
 /* Partial sums over the outer loop, x restricted to vertex indices [x0, x1)

@@ -328,3 +328,51 @@ def test_barbell_exceeds_u64_is_exact():
     g = oracle.Graph(*synth.complete(n))
     val = n * (n - 1) * (2 * comb(n - 1, 2)) ** 2
     assert val > 2**64 and g.count_barbell() == val
+
+
+# ------------------------------------------------------ NEXT-2: unpruned nests --
+@pytest.mark.parametrize("seed", range(8))
+def test_unpruned_nests_vs_ordered_bindings(seed):
+    """oracle_count_{triangles,4cliques}_unpruned (the Generic-Join on the
+    symmetric data) against brute-force ordered bindings."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(4, 14))
+    src, dst = synth.random_graph(n, int(rng.integers(0, n * n)), 300 + seed)
+    A = B.adjacency(src, dst)
+    g = oracle.Graph(src, dst)
+    try:
+        assert g.count_triangles_unpruned(2) == B.ordered_bindings(A, 3)
+        assert g.count_4cliques_unpruned(2) == B.ordered_bindings(A, 4)
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("p", [0.02, 0.1])
+def test_unpruned_triangles_trace(p):
+    src, dst = synth.er(300, p, 17)
+    A = B.adjacency(src, dst).astype(np.int64)
+    g = oracle.Graph(src, dst)
+    try:
+        assert g.count_triangles_unpruned() == int(np.trace(A @ A @ A))  # ordered closed walks of length 3
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 9, 40])
+def test_unpruned_kn_closed_forms(n):
+    g = oracle.Graph(*synth.complete(n))
+    try:
+        assert g.count_triangles_unpruned() == n * (n - 1) * (n - 2)  # 3! C(n, 3)
+        assert g.count_4cliques_unpruned() == 24 * comb(n, 4)
+    finally:
+        g.close()
+
+
+def test_unpruned_rmat_multiples():
+    src, dst = synth.rmat(11, 16, 41)
+    g = oracle.Graph(src, dst)
+    try:
+        assert g.count_triangles_unpruned() == 6 * g.count_triangles()
+        assert g.count_4cliques_unpruned() == 24 * g.count_4cliques()
+    finally:
+        g.close()
