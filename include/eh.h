@@ -153,6 +153,26 @@ int eh_count_lollipop(eh_graph* g, uint64_t out[2]);
 int eh_count_barbell(eh_graph* g, uint64_t out[2]);
 
 /*
+ * eh_count_triangles_unpruned -- NEXT-2: the triangle
+ * Generic-Join on the UNPRUNED data, i.e. the symmetric Edge relation (every
+ * undirected edge in both directions, ids by degree, no symmetry breaking:
+ * the "Default" rows of PAPER.md:1155-1236).  COUNT(*) then counts ordered
+ * bindings: 6 T ("a multiple of the former").  The
+ * symmetric trie (full sorted neighbour lists with their own set layouts, same
+ * tau) is built on the first call and kept by the handle (eh_symmetric_stats
+ * reports it).  Returns EH_COUNT_ERROR on error (EH_EINVAL, EH_ENOMEM, EH_ECUDA).
+ */
+uint64_t eh_count_triangles_unpruned(eh_graph* g);
+
+/*
+ * eh_symmetric_stats -- statistics of the symmetric trie (building it if
+ * needed): m_undirected = |E|, max_out_degree = max degree, alg_bytes_tri =
+ * B_tri of the unpruned nest (same formula over N(x)), device_bytes = its
+ * memory (not counted by eh_graph_stats).  Returns EH_OK or EH_E*.
+ */
+int eh_symmetric_stats(eh_graph* g, eh_stats* out);
+
+/*
  * eh_intersect -- the set operation "xs cap ys" of Table `lst:eh_operators`
  * (PAPER.md:515-516), with the paper's layout-dependent algorithms
  * (PAPER.md:628-642): each input gets the set-level layout (uint or bitset,

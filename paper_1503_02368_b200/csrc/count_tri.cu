@@ -48,7 +48,7 @@ constexpr int kWK_Warps = 8;
 // unless the id space is so large that the spans of N+(x) outgrow that bitmap
 // (C5: 2^26 ids), where 16-warp CTAs with a 64 KB structure win.
 constexpr uint32_t kCtaXCapMax = 16384;  // CTA kernel stages N+(x) in smem up to xcap = max |N+(x)|
-                                         // rounded up to 256, clamped to this
+constexpr uint32_t kCtaXCapNarrow = 4096; // rounded up to 256, clamped to these (wide / narrow shape)
 constexpr uint64_t kWideIds = 1ull << 24;  // n_active above this -> the wide shape
 constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor * |A| + 8
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
@@ -222,6 +222,9 @@ struct __align__(16) WarpSmem {
   uint8_t ord[kWarpMaxD];  // non-skip rows grouped by kind
 };
 
+// kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
+// N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
+template <bool kUnpruned>
 __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
@@ -247,11 +250,11 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
     __syncwarp();
     const XSet X = plan_xset(sm.tab, kWarpBmWords, sm.xs, d);
-    const uint32_t nrows = d - 1;
+    const uint32_t nrows = kUnpruned ? d : d - 1;
     bool need_x = false;  // only AND and STREAM rows read x's staged structure
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
-      const uint8_t kd = row_kind(y, nrows - i, X);
+      const uint8_t kd = row_kind(y, kUnpruned ? d : nrows - i, X);
       sm.yi[i] = y;
       sm.kind[i] = kd;
       need_x |= (kd == kAnd || kd == kStream);
@@ -273,7 +276,8 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
     __syncwarp();
     for (uint32_t r = grp; r < nr; r += 32 / kG) {
       const uint32_t i = sm.ord[r];
-      cnt += grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
+      cnt += kUnpruned ? grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
+                   : grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
-template <int kCtaWarps, int kTabW, int kXCap>  // kXCap > 0: compile-time staging capacity, else xcap_rt
+template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -318,14 +322,14 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
     __syncthreads();
     const XSet X = build_xset(tab, (d <= xcap) ? (uint32_t)kTabW : 0u, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
-    const uint32_t nrows = d - 1;
+    const uint32_t nrows = kUnpruned ? d : d - 1;
     uint32_t i = gid;
     YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      const uint32_t na = nrows - i;
-      cnt += grp_row(row_kind(y, na, X), col, bs, y, X, xs + i + 1, na, gl);
+      const uint32_t na = kUnpruned ? d : nrows - i;
+      cnt += grp_row(row_kind(y, na, X), col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       i = inext;
       y = ynext;
     }
@@ -336,10 +340,10 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
 }
 
 
-template <int NW, int TABW, int XCAP>
+template <int NW, int TABW, int XCAP, bool kUnpruned>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
-  auto k = k_tri_cta<NW, TABW, XCAP>;
+  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -349,9 +353,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   EH_LAUNCH("k_tri_cta");
 }
 
-}  // namespace
 
-uint64_t count_triangles(eh_graph* g) {
+template <bool kUnpruned>
+uint64_t count_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
   // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
@@ -359,23 +363,31 @@ uint64_t count_triangles(eh_graph* g) {
   const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
   const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
   if (nlarge) {
-    uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
+    const uint64_t cap = wide ? kCtaXCapMax : kCtaXCapNarrow;
+    uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
-    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096>(g, nsmall, nlarge, 0);
-    else if (wide) launch_cta<16, 16384, 0>(g, nsmall, nlarge, xcap);
-    else launch_cta<4, 2048, 0>(g, nsmall, nlarge, xcap);
+    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned>(g, nsmall, nlarge, 0);
+    else if (wide) launch_cta<16, 16384, 0, kUnpruned>(g, nsmall, nlarge, xcap);
+    else launch_cta<4, 2048, 0, kUnpruned>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(WarpSmem) * kWK_Warps;
-    EH_CUDA(cudaFuncSetAttribute(k_tri_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tri_warp<<<grid, kWK_Warps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    EH_CUDA(cudaFuncSetAttribute(k_tri_warp<kUnpruned>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_tri_warp<kUnpruned><<<grid, kWK_Warps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
     EH_LAUNCH("k_tri_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   return g->h_counter[0];
 }
+
+}  // namespace
+
+uint64_t count_triangles(eh_graph* g) { return count_impl<false>(g); }
+
+// NEXT-2: the unpruned nest over the symmetric trie (built on first use) = 6T.
+uint64_t count_triangles_unpruned(eh_graph* g) { return count_impl<true>(symmetric_trie(g)); }
 
 uint32_t tri_warp_max_degree() { return kWarpMaxD; }
 

@@ -44,6 +44,10 @@ void destroy(eh_graph* g) {
   cudaGetDevice(&prev);
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->sym) {
+    for (void* p : g->sym->owned) g->sym->alloc.release(p);
+    delete g->sym;
+  }
   for (void* p : g->owned) g->alloc.release(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
@@ -158,6 +162,33 @@ uint64_t eh_count_4cliques(eh_graph* g) {
     if (!g) eh::fail(EH_EINVAL, "eh_count_4cliques: NULL graph");
     DeviceGuard guard(g->device);
     return eh::count_4cliques(g);
+  });
+}
+
+uint64_t eh_count_triangles_unpruned(eh_graph* g) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_triangles_unpruned: NULL graph");
+    DeviceGuard guard(g->device);
+    return eh::count_triangles_unpruned(g);
+  });
+}
+
+int eh_symmetric_stats(eh_graph* g, eh_stats* out) {
+  return guarded<int>(EH_ECUDA, [&]() -> int {
+    if (!g || !out) eh::fail(EH_EINVAL, "eh_symmetric_stats: NULL argument");
+    DeviceGuard guard(g->device);
+    eh_graph* h = eh::symmetric_trie(g);
+    eh::compute_stats(h);
+    out->n_input = h->n_input;
+    out->m_undirected = h->m;
+    out->n_active = h->n_act;
+    out->max_out_degree = h->max_dplus;
+    out->n_bitset_sets = h->n_bitsets;
+    out->bitset_words = h->bs_words;
+    out->device_bytes = h->device_bytes;
+    out->alg_bytes_tri = h->alg_bytes_tri;
+    out->wedge_work = h->wedge_work;
+    return EH_OK;
   });
 }
 

@@ -213,6 +213,7 @@ struct eh_graph {
   uint64_t n_work[3] = {0, 0, 0};
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
+  eh_graph* sym = nullptr;  // NEXT-2: symmetric (unpruned) trie, built on first use (sym.cu)
 
   std::vector<void*> owned;  // every device allocation above
   uint64_t device_bytes = 0;
@@ -239,6 +240,9 @@ uint64_t count_4cliques(eh_graph* g);
 // count_pv.cu (NEXT-1): t(v) per rank into a device array; Lollipop / Barbell 128-bit counts
 void triangles_per_vertex(eh_graph* g, unsigned long long* d_t);
 void count_lollipop_barbell(eh_graph* g, bool barbell, uint64_t out2[2]);
+// sym.cu / count_tri.cu (NEXT-2): the symmetric trie (lazy) and the unpruned triangle nest (= 6T)
+eh_graph* symmetric_trie(eh_graph* g);
+uint64_t count_triangles_unpruned(eh_graph* g);
 // intersect.cu
 int64_t intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);
 }  // namespace eh

@@ -67,6 +67,10 @@ def lib():
         L.eh_count_triangles.restype = u64
         L.eh_count_4cliques.argtypes = [vp]
         L.eh_count_4cliques.restype = u64
+        L.eh_count_triangles_unpruned.argtypes = [vp]
+        L.eh_count_triangles_unpruned.restype = u64
+        L.eh_symmetric_stats.argtypes = [vp, ctypes.POINTER(EHStats)]
+        L.eh_symmetric_stats.restype = ctypes.c_int
         L.eh_triangles_per_vertex.argtypes = [vp, vp]
         L.eh_triangles_per_vertex.restype = ctypes.c_int
         for name in ("eh_count_lollipop", "eh_count_barbell"):
@@ -91,7 +95,8 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("eh_load_edges", "eh_load_edges_ex", "eh_count_triangles", "eh_count_4cliques",
-                    "eh_triangles_per_vertex", "eh_count_lollipop", "eh_count_barbell", "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
+                    "eh_count_triangles_unpruned", "eh_symmetric_stats", "eh_triangles_per_vertex",
+                    "eh_count_lollipop", "eh_count_barbell", "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
                     "eh_last_error")
 
 
@@ -214,6 +219,20 @@ class Graph:
         if r == EH_COUNT_ERROR:
             _raise()
         return int(r)
+
+    def count_triangles_unpruned(self) -> int:
+        """NEXT-2: the triangle Generic-Join on the symmetric (unpruned) data = 6T (eh_count_triangles_unpruned)."""
+        r = lib().eh_count_triangles_unpruned(self._h)
+        if r == EH_COUNT_ERROR:
+            _raise()
+        return int(r)
+
+    def symmetric_stats(self) -> Stats:
+        """Statistics of the symmetric trie (eh_symmetric_stats)."""
+        st = EHStats()
+        if lib().eh_symmetric_stats(self._h, ctypes.byref(st)) != EH_OK:
+            _raise()
+        return Stats(**{f: int(getattr(st, f)) for f, _ in EHStats._fields_})
 
     def triangles_per_vertex(self, out=None):
         """t(v) per rank (eh_triangles_per_vertex); rank r is original id export()[2][r].
