@@ -50,6 +50,8 @@ constexpr int kWK_Warps = 8;
 constexpr uint32_t kCtaXCapMax = 16384;  // CTA kernel stages N+(x) in smem up to xcap = max |N+(x)|
 constexpr uint32_t kCtaXCapNarrow = 4096; // rounded up to 256, clamped to these (wide / narrow shape)
 constexpr uint64_t kWideIds = 1ull << 24;  // n_active above this -> the wide shape
+constexpr uint32_t kRowsPerItem = 1024;    // NEXT-2: rows of one CTA work item
+constexpr uint64_t kHubBitmapBudget = 4ull << 30;  // NEXT-2: device bytes for the hub bitmaps
 constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor * |A| + 8
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -169,6 +171,27 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
   return kStream;
 }
 
+// Unpruned rows (NEXT-2) meet every combination of |A| = d(x) and |N(y)|
+// (hubs on both sides), so the choice uses explicit costs: PROBE a bit tests,
+// STREAM |N(y)| lookups in x's structure (log2 d when it is the sorted list),
+// SEARCH a binary searches of N(y), AND as above.
+__device__ __forceinline__ uint8_t row_kind_unpruned(const YInfo& y, uint32_t a, const XSet& X) {
+  if (a == 0 || y.len == 0) return kSkip;
+  const uint32_t lgx = (X.mode == kSorted) ? (32 - __clz(X.d)) : 1u;
+  const uint64_t stream = (uint64_t)y.len * lgx;
+  if (y.c1 > y.c0) {
+    if (X.mode == kBitmap) {
+      const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
+      const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
+      if (hi <= lo) return kSkip;
+      if (hi - lo <= kAndFactor * a + 8) return kAnd;
+    }
+    return (stream < a) ? kStream : kProbe;
+  }
+  const uint64_t search = (uint64_t)a * (32 - __clz(y.len)) * 4;
+  return (search < stream) ? kSearchGlobal : kStream;
+}
+
 // ---- group-level row bodies: kG lanes, gl = lane within the group --------
 __device__ __forceinline__ uint32_t and4(const uint4 u, const uint4 v) {
   return __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
@@ -254,7 +277,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
     bool need_x = false;  // only AND and STREAM rows read x's staged structure
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
-      const uint8_t kd = row_kind(y, kUnpruned ? d : nrows - i, X);
+      const uint8_t kd = kUnpruned ? row_kind_unpruned(y, d, X) : row_kind(y, nrows - i, X);
       sm.yi[i] = y;
       sm.kind[i] = kd;
       need_x |= (kd == kAnd || kd == kStream);
@@ -294,7 +317,12 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
                                                             const uint32_t* __restrict__ work, uint64_t nwork,
-                                                            unsigned long long* __restrict__ ctr, uint32_t xcap_rt) {
+                                                            unsigned long long* __restrict__ ctr, uint32_t xcap_rt,
+                                                            const unsigned long long* __restrict__ items,
+                                                            const uint32_t* __restrict__ hslot,
+                                                            uint32_t* __restrict__ hub_bm, uint32_t hub_words) {
+  // kUnpruned: work items are (x << 32 | first row) over row ranges of kRowsPerItem
+  // (hub lists of the symmetric trie would otherwise leave one CTA with 10^5 rows)
   const uint32_t xcap = kXCap > 0 ? (uint32_t)kXCap : xcap_rt;
   extern __shared__ __align__(16) uint32_t dsm[];
   uint32_t* xs_s = dsm;             // xcap
@@ -309,7 +337,16 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
     __syncthreads();
     const unsigned long long wi = s_wi;
     if (wi >= nwork) break;
-    const uint32_t x = __ldg(work + wi);
+    uint32_t x, r0 = 0, slot = 0xFFFFFFFFu;
+    if (kUnpruned) {  // item = (index in the work list << 32) | first row
+      const unsigned long long it = __ldg(items + wi);
+      const uint32_t k = (uint32_t)(it >> 32);
+      x = __ldg(work + k);
+      r0 = (uint32_t)it;
+      if (hslot) slot = __ldg(hslot + k);
+    } else {
+      x = __ldg(work + wi);
+    }
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
@@ -320,16 +357,30 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
       xs = xs_s;
     }
     __syncthreads();
-    const XSet X = build_xset(tab, (d <= xcap) ? (uint32_t)kTabW : 0u, xs, d, threadIdx.x, blockDim.x);
+    XSet X;
+    if (kUnpruned && slot != 0xFFFFFFFFu) {  // hub: its bitmap over the whole id space, built once, L2-resident
+      X.tab = hub_bm + (uint64_t)slot * hub_words;
+      X.xs = xs;
+      X.mode = kBitmap;
+      X.lo = 0;
+      X.nbits = hub_words * 32;
+      X.hshift = X.hmask = 0;
+      X.d = d;
+      X.amin = xs[0];
+      X.amax = xs[d - 1];
+    } else {
+      X = build_xset(tab, (d <= xcap) ? (uint32_t)kTabW : 0u, xs, d, threadIdx.x, blockDim.x);
+    }
     __syncthreads();
-    const uint32_t nrows = kUnpruned ? d : d - 1;
-    uint32_t i = gid;
+    const uint32_t nrows = kUnpruned ? min(d, r0 + kRowsPerItem) : d - 1;
+    uint32_t i = r0 + gid;
     YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
       const uint32_t na = kUnpruned ? d : nrows - i;
-      cnt += grp_row(row_kind(y, na, X), col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+      const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind(y, na, X);
+      cnt += grp_row(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       i = inext;
       y = ynext;
     }
@@ -340,17 +391,97 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
 }
 
 
+// NEXT-2 row-range items: x with d rows becomes ceil(d / kRowsPerItem) items.
+__global__ void k_item_count(const uint4* __restrict__ desc, const uint32_t* __restrict__ work, uint64_t n,
+                             uint32_t* __restrict__ cnt) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    cnt[k] = (desc[work[k]].y + kRowsPerItem - 1) / kRowsPerItem;
+}
+__global__ void k_item_emit(const uint32_t* __restrict__ work, uint64_t n, const uint32_t* __restrict__ cnt,
+                            const uint64_t* __restrict__ off, unsigned long long* __restrict__ items) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    for (uint32_t c = 0; c < cnt[k]; ++c) items[off[k] + c] = ((unsigned long long)k << 32) | (c * kRowsPerItem);
+}
+
+// NEXT-2 hubs (|N(x)| > xcap): one bitmap of N(x) over the whole id space per hub.
+struct HubPred {
+  const uint4* desc;
+  const uint32_t* work;
+  uint32_t xcap;
+  __device__ bool operator()(uint64_t k) const { return desc[work[k]].y > xcap; }
+};
+struct HubEmit {
+  uint32_t* hslot;
+  uint32_t* hubk;
+  __device__ void operator()(uint64_t pos, uint64_t k) const {
+    hslot[k] = (uint32_t)pos;
+    hubk[pos] = (uint32_t)k;
+  }
+};
+__global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
+                           const uint32_t* __restrict__ work, const uint32_t* __restrict__ hubk, uint32_t words,
+                           uint32_t* __restrict__ bm) {
+  const uint32_t h = blockIdx.x;
+  const uint4 d = desc[work[hubk[h]]];
+  uint32_t* b = bm + (uint64_t)h * words;
+  for (uint32_t k = threadIdx.x; k < d.y; k += blockDim.x) {
+    const uint32_t e = col[(uint64_t)d.x * 4 + k];
+    atomicOr(&b[e >> 5], 1u << (e & 31));
+  }
+}
+
 template <int NW, int TABW, int XCAP, bool kUnpruned>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
   auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
+  cudaStream_t s = g->stream;
+  DBuf<unsigned long long> items;
+  DBuf<uint32_t> hslot, hubk, hub_bm;
+  uint32_t hub_words = 0;
+  uint64_t nitems = nlarge;
+  if (kUnpruned) {
+    hslot = DBuf<uint32_t>(g->alloc, nlarge);
+    hubk = DBuf<uint32_t>(g->alloc, nlarge);
+    hub_words = (uint32_t)((g->n_act + 127) / 128 * 4);
+    // hubs = lists above the staging capacity, raised until their bitmaps fit the
+    // budget; lists above xcap that are not hubs use the global sorted list
+    uint64_t hub_min = xcap, nh = 0;
+    for (;;) {
+      EH_CUDA(cudaMemsetAsync(hslot.p, 0xFF, nlarge * 4, s));
+      nh = select_if(nlarge, HubPred{g->desc, g->work + nsmall, (uint32_t)std::min<uint64_t>(hub_min, UINT32_MAX)},
+                     HubEmit{hslot.p, hubk.p}, g->alloc, s);
+      if (nh * hub_words * 4ull <= kHubBitmapBudget || hub_min > g->max_dplus) break;
+      hub_min *= 2;
+    }
+    if (nh * hub_words * 4ull > kHubBitmapBudget) {  // not even the largest lists fit: no hub bitmaps
+      EH_CUDA(cudaMemsetAsync(hslot.p, 0xFF, nlarge * 4, s));
+      nh = 0;
+    }
+    if (nh) {
+      hub_bm = DBuf<uint32_t>(g->alloc, nh * hub_words);
+      EH_CUDA(cudaMemsetAsync(hub_bm.p, 0, hub_bm.bytes(), s));
+      k_hub_fill<<<(unsigned)nh, 1024, 0, s>>>(g->desc, g->col, g->work + nsmall, hubk.p, hub_words, hub_bm.p);
+      EH_LAUNCH("k_hub_fill");
+    }
+    DBuf<uint32_t> cnt(g->alloc, nlarge);
+    DBuf<uint64_t> off(g->alloc, nlarge + 1), tot(g->alloc, 1);
+    k_item_count<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->desc, g->work + nsmall, nlarge, cnt.p);
+    EH_LAUNCH("k_item_count");
+    scan_exclusive_u32(cnt.p, off.p, nlarge, tot.p, g->alloc, s);
+    nitems = read_scalar(tot.p, s);
+    items = DBuf<unsigned long long>(g->alloc, nitems);
+    k_item_emit<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->work + nsmall, nlarge, cnt.p, off.p, items.p);
+    EH_LAUNCH("k_item_emit");
+  }
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, smem));
-  const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-  k<<<grid, NW * 32, smem, g->stream>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, g->d_counter, xcap);
+  const unsigned grid = (unsigned)std::min<uint64_t>(nitems, (uint64_t)kSMs * std::max(1, per_sm));
+  k<<<grid, NW * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nitems, g->d_counter, xcap, items.p,
+                                kUnpruned ? hslot.p : nullptr, hub_bm.p, hub_words);
   EH_LAUNCH("k_tri_cta");
+  if (kUnpruned) EH_CUDA(cudaStreamSynchronize(s));  // items is released on return
 }
 
 
@@ -359,11 +490,13 @@ uint64_t count_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
   // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
-  const bool wide = g->n_act > kWideIds;
+  // the symmetric trie's hub lists always take the wide shape (measured: C3 2.70 -> 1.27 s)
+  const bool wide = g->n_act > kWideIds || kUnpruned;
   const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
   const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
   if (nlarge) {
-    const uint64_t cap = wide ? kCtaXCapMax : kCtaXCapNarrow;
+    // unpruned: lists above 4096 use the global hub bitmaps (measured: C3 0.93 -> 0.42 s)
+    const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
     uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
     if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned>(g, nsmall, nlarge, 0);

@@ -18,6 +18,7 @@ PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6538.6
 NEXT1 = "--next1" in sys.argv
+NEXT2 = "--next2" in sys.argv
 names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"]
 reps = 5
 for name in names:
@@ -80,6 +81,35 @@ for name in names:
         pv_bytes = stats.alg_bytes_tri + 8 * stats.n_active  # B_tri reads + the t(v) array
         res.update(pv_ms=pv, lollipop_ms=statistics.median(lols), barbell_ms=statistics.median(bars),
                    pv_alg_bytes=pv_bytes, pv_gbs=pv_bytes / pv / 1e6, pv_roofline_frac=pv_bytes / pv / 1e6 / PEAK)
+    if NEXT2:  # unpruned nest on the symmetric trie, default and all-uint (-R)
+        for label, kw in (("", {}), ("_R", {"all_uint": True})):
+            with torch.cuda.stream(st):
+                g = eh.Graph(s, d, stream=st, **kw)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                sst = g.symmetric_stats()  # builds the symmetric trie (+ its statistics)
+                e1.record(st)
+                st.synchronize()
+                build_ms = e0.elapsed_time(e1)
+                u = g.count_triangles_unpruned()
+                us, ps = [], []
+                for r in range(reps):
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                    ev[0].record(st)
+                    g.count_triangles_unpruned()
+                    ev[1].record(st)
+                    g.count_triangles()
+                    ev[2].record(st)
+                    st.synchronize()
+                    us.append(ev[0].elapsed_time(ev[1]))
+                    ps.append(ev[1].elapsed_time(ev[2]))
+                g.close()
+            um = statistics.median(us)
+            res.update({f"unpruned{label}": u, f"unpruned{label}_ms": um, f"pruned{label}_ms": statistics.median(ps),
+                        f"sym_build{label}_ms": build_ms, f"B_sym{label}": sst.alg_bytes_tri,
+                        f"unpruned{label}_gbs": sst.alg_bytes_tri / um / 1e6,
+                        f"unpruned{label}_frac": sst.alg_bytes_tri / um / 1e6 / PEAK,
+                        f"sym_bitset_sets{label}": sst.n_bitset_sets, f"sym_max_degree": sst.max_out_degree})
     print(json.dumps(res), flush=True)
     del s, d
     torch.cuda.empty_cache()

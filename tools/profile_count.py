@@ -16,7 +16,7 @@ if os.environ.get("TRI_LIB"):  # dev: profile another build of the library
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
-ap.add_argument("--query", default="tri", choices=["tri", "k4", "pv", "lollipop"])
+ap.add_argument("--query", default="tri", choices=["tri", "k4", "pv", "lollipop", "unpruned"])
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tau", type=int, default=0)
 ap.add_argument("--small", type=int, default=0)
@@ -29,6 +29,7 @@ with eh.Graph(src, dst, tau=a.tau, bin_small_max=a.small or a.small_max, bin_lar
     for _ in range(a.reps):
         t0 = time.perf_counter()
         c = {"tri": g.count_triangles, "k4": g.count_4cliques, "lollipop": g.count_lollipop,
-             "pv": lambda: int(g.triangles_per_vertex().sum())}[a.query]()
+             "pv": lambda: int(g.triangles_per_vertex().sum()),
+             "unpruned": g.count_triangles_unpruned}[a.query]()
         print(f"{a.query} = {c}  {1e3 * (time.perf_counter() - t0):.2f} ms", flush=True)
     print(st, flush=True)
