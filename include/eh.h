@@ -165,6 +165,14 @@ int eh_count_barbell(eh_graph* g, uint64_t out[2]);
 uint64_t eh_count_triangles_unpruned(eh_graph* g);
 
 /*
+ * eh_count_4cliques_unpruned -- NEXT-2: the 4-clique Generic-Join on the
+ * unpruned (symmetric) data, attribute order x, y, z, w: 24 K4.  Same
+ * symmetric trie.  Lists above 1024 elements take a generic per-warp path that
+ * is slow on skewed graphs (hub x hub pairs).  Returns EH_COUNT_ERROR on error.
+ */
+uint64_t eh_count_4cliques_unpruned(eh_graph* g);
+
+/*
  * eh_symmetric_stats -- statistics of the symmetric trie (building it if
  * needed): m_undirected = |E|, max_out_degree = max degree, alg_bytes_tri =
  * B_tri of the unpruned nest (same formula over N(x)), device_bytes = its

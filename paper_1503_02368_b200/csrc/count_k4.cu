@@ -85,12 +85,15 @@ __device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a) {
   return kKStream;
 }
 
-// Fill row i of L (stride W words) with the 8-lane group's lane gl.
+// Fill row i of L (stride W words) with the 8-lane group's lane gl.  kU
+// (NEXT-2, unpruned nest on the symmetric trie): the row is all of
+// N(x) cap N(x_i), not only the part after x_i.
+template <bool kU>
 __device__ __forceinline__ void fill_row(uint8_t kd, const uint32_t* __restrict__ col, const uint32_t* __restrict__ bs,
                                          const YInfo& y, const uint32_t* xs, uint32_t d, uint32_t i, const LocalHash& H,
                                          uint32_t* Lrow, uint32_t gl) {
   if (kd == kKProbe) {
-    for (uint32_t j = i + 1 + gl; j < d; j += kG)
+    for (uint32_t j = (kU ? 0 : i + 1) + gl; j < d; j += kG)
       if (probe_bits(bs, y, xs[j])) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
   } else if (kd == kKStream) {
     const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
@@ -109,7 +112,7 @@ __device__ __forceinline__ void fill_row(uint8_t kd, const uint32_t* __restrict_
       if (j >= 0) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
     }
   } else if (kd == kKSearch) {
-    for (uint32_t j = i + 1 + gl; j < d; j += kG)
+    for (uint32_t j = (kU ? 0 : i + 1) + gl; j < d; j += kG)
       if (gmem_search(col + (uint64_t)y.list * 4, y.len, xs[j])) atomicOr(&Lrow[j >> 5], 1u << (j & 31));
   }
 }
@@ -125,6 +128,7 @@ struct __align__(16) K4WarpSmem {
   uint8_t ord[kWMaxD];
 };
 
+template <bool kU>
 __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
@@ -150,11 +154,11 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
     for (uint32_t k = lane; k < d * kWW; k += 32) sm.L[k] = 0u;
     __syncwarp();
     const LocalHash H = build_local_hash<false>(sm.hkeys, sm.hidx, sm.xs, d, lane, 32);
-    const uint32_t nrows = d - 1;
+    const uint32_t nrows = kU ? d : d - 1;
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
       sm.yi[i] = y;
-      sm.kind[i] = k4_kind(y, nrows - i);
+      sm.kind[i] = k4_kind(y, kU ? d : nrows - i);
     }
     __syncwarp();
     uint32_t nr = 0;
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
     __syncwarp();
     for (uint32_t r = lane / kG; r < nr; r += 32 / kG) {
       const uint32_t i = sm.ord[r];
-      fill_row(sm.kind[i], col, bs, sm.yi[i], sm.xs, d, i, H, sm.L + i * kWW, lane % kG);
+      fill_row<kU>(sm.kind[i], col, bs, sm.yi[i], sm.xs, d, i, H, sm.L + i * kWW, lane % kG);
     }
     __syncwarp();
     // bit-parallel innermost loop: 4-lane groups, lane q holds word q of row i
@@ -186,8 +190,8 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
           const uint32_t b = __ffs(wb) - 1;
           wb &= wb - 1;
           const uint32_t j = kk * 32 + b;
-          if (q >= kk && q < W) {
-            const uint32_t m = (q == kk) ? ~((2u << b) - 1u) : 0xFFFFFFFFu;
+          if (kU ? q < W : (q >= kk && q < W)) {  // unpruned: all w, else w after z
+            const uint32_t m = (kU || q != kk) ? 0xFFFFFFFFu : ~((2u << b) - 1u);
             cnt += __popc(li & sm.L[j * kWW + q] & m);
           }
         }
@@ -200,6 +204,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
 }
 
 // ------------------------------------------------------------- CTA kernel --
+template <bool kU>
 __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
@@ -237,13 +242,13 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
     __syncthreads();
     const LocalHash H = build_local_hash<true>(hkeys, hidx, xs, d, threadIdx.x, blockDim.x);
     __syncthreads();
-    const uint32_t nrows = d - 1;
+    const uint32_t nrows = kU ? d : d - 1;
     uint32_t i = gid;
     YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      fill_row(k4_kind(y, nrows - i), col, bs, y, xs, d, i, H, L + i * S, gl);
+      fill_row<kU>(k4_kind(y, kU ? d : nrows - i), col, bs, y, xs, d, i, H, L + i * S, gl);
       i = inext;
       y = ynext;
     }
@@ -269,8 +274,13 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
         const uint32_t j = jl[e];
         const uint32_t kk = j >> 5;
         const uint32_t* Lj = L + j * S;
-        uint32_t acc = __popc(Li[kk] & Lj[kk] & ~((2u << (j & 31)) - 1u));
-        for (uint32_t k = kk + 1; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
+        uint32_t acc = 0;
+        if (kU) {  // all w
+          for (uint32_t k = 0; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
+        } else {   // w after z
+          acc = __popc(Li[kk] & Lj[kk] & ~((2u << (j & 31)) - 1u));
+          for (uint32_t k = kk + 1; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
+        }
         cnt += acc;
       }
       __syncwarp();
@@ -285,11 +295,31 @@ constexpr size_t kCtaSmemK4 =
     (size_t)(kCMaxD + kCHash + kCHash / 2 + kCMaxD * (kCMaxD / 32 + 1)) * 4 + (size_t)kCWarps * kCMaxD * 2;
 
 // ------------------------------------------- fallback: |N+(x)| > kCMaxD --
-// P = N+(x) after y cap N+(y) materialised per warp (global scratch), then
-// for z in P: |P after z cap N+(z)| by membership probes.
+// Rows (x, y = x_i) of the big x are flattened into one index space (prefix
+// sums of their row counts) and taken one per warp: P = N+(x) after y cap
+// N+(y) (kU: all of N(x) cap N(y)) materialised in the warp's global scratch,
+// then for z in P: |P after z cap N+(z)| (kU: all of P) by membership probes.
+struct BigPred {
+  const uint4* desc;
+  const uint32_t* work;
+  __device__ bool operator()(uint64_t k) const { return desc[work[k]].y > (uint32_t)kCMaxD; }
+};
+struct BigEmit {
+  const uint4* desc;
+  const uint32_t* work;
+  uint32_t* bx;
+  uint32_t* brows;
+  __device__ void operator()(uint64_t pos, uint64_t k) const {
+    bx[pos] = work[k];
+    brows[pos] = desc[work[k]].y;
+  }
+};
+
+template <bool kU>
 __global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
-                                                 const uint32_t* __restrict__ bs, const uint32_t* __restrict__ work,
-                                                 uint64_t nwork, uint32_t* __restrict__ pscratch, uint32_t pstride,
+                                                 const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bx,
+                                                 const uint64_t* __restrict__ boff, uint64_t nbig, uint64_t nrows,
+                                                 uint32_t* __restrict__ pscratch, uint32_t pstride,
                                                  unsigned long long* __restrict__ ctr) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -297,71 +327,89 @@ __global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, 
   uint32_t* P = pscratch + gw * pstride;
   unsigned long long cnt = 0;
   for (;;) {
-    unsigned long long wi = 0;
-    if (lane == 0) wi = atomicAdd(&ctr[3], 1ull);
-    wi = __shfl_sync(kFull, wi, 0);
-    if (wi >= nwork) break;
-    const uint32_t x = __ldg(work + wi);
+    unsigned long long r = 0;
+    if (lane == 0) r = atomicAdd(&ctr[3], 1ull);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= nrows) break;
+    uint64_t lo = 0, hi = nbig;  // the big x whose rows contain r: last boff[k] <= r
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (boff[mid] <= r) lo = mid; else hi = mid;
+    }
+    const uint32_t x = bx[lo], i = (uint32_t)(r - boff[lo]);
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;
-    if (d <= (uint32_t)kCMaxD) continue;
     const uint32_t* xs = col + (uint64_t)dx.x * 4;
-    for (uint32_t i = 0; i + 2 < d; ++i) {
-      const SetRef sy = set_of(desc, col, bs, xs[i]);
-      if (sy.len < 2) continue;
-      uint32_t np = 0;
-      for (uint32_t j0 = i + 1; j0 < d; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const uint32_t e = (j < d) ? xs[j] : 0u;
-        const uint32_t hit = (j < d) ? member(sy, e) : 0u;
-        const unsigned mask = __ballot_sync(kFull, hit);
-        if (hit) P[np + __popc(mask & lt)] = e;
-        np += __popc(mask);
-      }
-      __syncwarp();
-      for (uint32_t t = 0; t + 1 < np; ++t) {
-        const SetRef sz = set_of(desc, col, bs, P[t]);
-        if (sz.len == 0) continue;
-        for (uint32_t k = t + 1 + lane; k < np; k += 32) cnt += member(sz, P[k]);
-      }
-      __syncwarp();
+    if (!kU && i + 2 >= d) continue;
+    const SetRef sy = set_of(desc, col, bs, xs[i]);
+    if (sy.len < 2) continue;
+    uint32_t np = 0;
+    for (uint32_t j0 = kU ? 0 : i + 1; j0 < d; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t e = (j < d) ? xs[j] : 0u;
+      const uint32_t hit = (j < d) ? member(sy, e) : 0u;
+      const unsigned mask = __ballot_sync(kFull, hit);
+      if (hit) P[np + __popc(mask & lt)] = e;
+      np += __popc(mask);
     }
+    __syncwarp();
+    for (uint32_t t = 0; t < np; ++t) {
+      const SetRef sz = set_of(desc, col, bs, P[t]);
+      if (sz.len == 0) continue;
+      for (uint32_t k = (kU ? 0 : t + 1) + lane; k < np; k += 32) cnt += member(sz, P[k]);
+    }
+    __syncwarp();
   }
   cnt = warp_sum(cnt);
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
-}  // namespace
-
-uint64_t count_4cliques(eh_graph* g) {
+template <bool kU>
+uint64_t k4_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
   const uint64_t nlarge = g->n_work[2];
   const uint32_t* wl = g->work + nsmall;
   if (nlarge) {
-    EH_CUDA(cudaFuncSetAttribute(k_k4_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemK4));
+    EH_CUDA(cudaFuncSetAttribute(k_k4_cta<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemK4));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-    k_k4_cta<<<grid, kCWarps * 32, kCtaSmemK4, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter);
+    k_k4_cta<kU><<<grid, kCWarps * 32, kCtaSmemK4, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter);
     EH_LAUNCH("k_k4_cta");
     if (g->max_dplus > (uint64_t)kCMaxD) {
-      const unsigned gb = (unsigned)kSMs * 4;
+      DBuf<uint32_t> bx(g->alloc, nlarge), brows(g->alloc, nlarge);
+      const uint64_t nbig = select_if(nlarge, BigPred{g->desc, wl}, BigEmit{g->desc, wl, bx.p, brows.p}, g->alloc, s);
+      DBuf<uint64_t> boff(g->alloc, nbig + 1), tot(g->alloc, 1);
+      scan_exclusive_u32(brows.p, boff.p, nbig, tot.p, g->alloc, s);
+      const uint64_t nrows = read_scalar(tot.p, s);
+      const unsigned gb = (unsigned)kSMs * 8;
       const uint32_t stride = (uint32_t)g->max_dplus;
       DBuf<uint32_t> scratch(g->alloc, (size_t)gb * 4 * stride);
-      k_k4_big<<<gb, 128, 0, s>>>(g->desc, g->col, g->bs, wl, nlarge, scratch.p, stride, g->d_counter);
+      k_k4_big<kU><<<gb, 128, 0, s>>>(g->desc, g->col, g->bs, bx.p, boff.p, nbig, nrows, scratch.p, stride,
+                                      g->d_counter);
       EH_LAUNCH("k_k4_big");
+      EH_CUDA(cudaStreamSynchronize(s));  // scratch is released on return
     }
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(K4WarpSmem) * kWWarps;
-    EH_CUDA(cudaFuncSetAttribute(k_k4_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_k4_warp<<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    EH_CUDA(cudaFuncSetAttribute(k_k4_warp<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_k4_warp<kU><<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
     EH_LAUNCH("k_k4_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   return g->h_counter[0];
 }
+
+}  // namespace
+
+uint64_t count_4cliques(eh_graph* g) { return k4_impl<false>(g); }
+
+// NEXT-2: the unpruned 4-clique nest over the symmetric trie = 24 K4.  Hub
+// lists (> 1024) take the generic per-warp fallback, which is slow on skewed
+// graphs (DESIGN.md NEXT-2).
+uint64_t count_4cliques_unpruned(eh_graph* g) { return k4_impl<true>(symmetric_trie(g)); }
 
 }  // namespace eh

@@ -173,6 +173,14 @@ uint64_t eh_count_triangles_unpruned(eh_graph* g) {
   });
 }
 
+uint64_t eh_count_4cliques_unpruned(eh_graph* g) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_4cliques_unpruned: NULL graph");
+    DeviceGuard guard(g->device);
+    return eh::count_4cliques_unpruned(g);
+  });
+}
+
 int eh_symmetric_stats(eh_graph* g, eh_stats* out) {
   return guarded<int>(EH_ECUDA, [&]() -> int {
     if (!g || !out) eh::fail(EH_EINVAL, "eh_symmetric_stats: NULL argument");

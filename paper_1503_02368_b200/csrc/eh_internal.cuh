@@ -243,6 +243,7 @@ void count_lollipop_barbell(eh_graph* g, bool barbell, uint64_t out2[2]);
 // sym.cu / count_tri.cu (NEXT-2): the symmetric trie (lazy) and the unpruned triangle nest (= 6T)
 eh_graph* symmetric_trie(eh_graph* g);
 uint64_t count_triangles_unpruned(eh_graph* g);
+uint64_t count_4cliques_unpruned(eh_graph* g);  // count_k4.cu: = 24 K4
 // intersect.cu
 int64_t intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t* out);
 }  // namespace eh

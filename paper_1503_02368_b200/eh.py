@@ -67,8 +67,9 @@ def lib():
         L.eh_count_triangles.restype = u64
         L.eh_count_4cliques.argtypes = [vp]
         L.eh_count_4cliques.restype = u64
-        L.eh_count_triangles_unpruned.argtypes = [vp]
-        L.eh_count_triangles_unpruned.restype = u64
+        for name in ("eh_count_triangles_unpruned", "eh_count_4cliques_unpruned"):
+            getattr(L, name).argtypes = [vp]
+            getattr(L, name).restype = u64
         L.eh_symmetric_stats.argtypes = [vp, ctypes.POINTER(EHStats)]
         L.eh_symmetric_stats.restype = ctypes.c_int
         L.eh_triangles_per_vertex.argtypes = [vp, vp]
@@ -95,7 +96,8 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("eh_load_edges", "eh_load_edges_ex", "eh_count_triangles", "eh_count_4cliques",
-                    "eh_count_triangles_unpruned", "eh_symmetric_stats", "eh_triangles_per_vertex",
+                    "eh_count_triangles_unpruned", "eh_count_4cliques_unpruned", "eh_symmetric_stats",
+                    "eh_triangles_per_vertex",
                     "eh_count_lollipop", "eh_count_barbell", "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
                     "eh_last_error")
 
@@ -223,6 +225,13 @@ class Graph:
     def count_triangles_unpruned(self) -> int:
         """NEXT-2: the triangle Generic-Join on the symmetric (unpruned) data = 6T (eh_count_triangles_unpruned)."""
         r = lib().eh_count_triangles_unpruned(self._h)
+        if r == EH_COUNT_ERROR:
+            _raise()
+        return int(r)
+
+    def count_4cliques_unpruned(self) -> int:
+        """NEXT-2: the 4-clique Generic-Join on the symmetric (unpruned) data = 24 K4 (eh_count_4cliques_unpruned)."""
+        r = lib().eh_count_4cliques_unpruned(self._h)
         if r == EH_COUNT_ERROR:
             _raise()
         return int(r)

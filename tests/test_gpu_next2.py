@@ -105,3 +105,42 @@ def test_configs_vs_oracle_golden(name, golden_dir):
     src, dst = synth.CONFIGS[name].generate()
     assert str(synth.checksum(src, dst)) == gold["checksum"]
     assert _gpu(src, dst)[0] == 6 * gold["triangles"]
+
+
+# ------------------------------------------------------------ unpruned 4-clique --
+def _k4u(src, dst, **kw):
+    with eh.Graph(src, dst, **kw) as g:
+        return g.count_4cliques_unpruned(), g.count_4cliques()
+
+
+@pytest.mark.parametrize("n", [0, 3, 4, 5, 12, 64, 129, 200])
+def test_k4_unpruned_kn(n):
+    from math import comb
+    assert _k4u(*synth.complete(n))[0] == 24 * comb(n, 4)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_k4_unpruned_vs_oracle(seed):
+    rng = np.random.default_rng(500 + seed)
+    if seed % 2:
+        src, dst = synth.rmat(int(rng.integers(6, 11)), 16, 500 + seed)
+    else:
+        src, dst = synth.er(int(rng.integers(20, 400)), float(rng.choice([0.02, 0.1, 0.3])), 500 + seed)
+    u, k = _k4u(src, dst)
+    og = oracle.Graph(src, dst)
+    try:
+        assert u == og.count_4cliques_unpruned() == 24 * k
+    finally:
+        og.close()
+
+
+def test_k4_unpruned_hub_fallback():
+    # complete graph K_1100: every list exceeds the 1024 bit-matrix limit (generic path)
+    from math import comb
+    assert _k4u(*synth.complete(1100))[0] == 24 * comb(1100, 4)
+
+
+@pytest.mark.parametrize("kw", [dict(tau=2), dict(all_uint=True), dict(bin_large_min=1)])
+def test_k4_unpruned_invariance(kw):
+    src, dst = synth.rmat(11, 16, 77)
+    assert _k4u(src, dst)[0] == _k4u(src, dst, **kw)[0] == 24 * _k4u(src, dst)[1]

@@ -105,6 +105,17 @@ for name in names:
                     ps.append(ev[1].elapsed_time(ev[2]))
                 g.close()
             um = statistics.median(us)
+            if label == "" and (cfg.query == "4cliques" or name in ("C1", "C2")):
+                with torch.cuda.stream(st):
+                    g = eh.Graph(s, d, stream=st)
+                    g.symmetric_stats()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    res["k4_unpruned"] = g.count_4cliques_unpruned()
+                    e1.record(st)
+                    st.synchronize()
+                    res["k4_unpruned_ms"] = e0.elapsed_time(e1)
+                    g.close()
             res.update({f"unpruned{label}": u, f"unpruned{label}_ms": um, f"pruned{label}_ms": statistics.median(ps),
                         f"sym_build{label}_ms": build_ms, f"B_sym{label}": sst.alg_bytes_tri,
                         f"unpruned{label}_gbs": sst.alg_bytes_tri / um / 1e6,
