@@ -81,7 +81,7 @@ __device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a) {
   if (a == 0 || y.len == 0) return kKSkip;
   if (y.c1 > y.c0) return kKProbe;
   const uint32_t lg = 32 - __clz(y.len);
-  if ((uint64_t)a * lg * 4 < y.len) return kKSearch;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kKSearch;
   return kKStream;
 }
 

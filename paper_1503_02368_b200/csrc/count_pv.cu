@@ -141,7 +141,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XI
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if ((uint64_t)a * lg * 4 < y.len) return kSearch;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kSearch;
   return kStream;
 }
 

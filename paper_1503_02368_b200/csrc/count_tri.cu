@@ -167,7 +167,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if ((uint64_t)a * lg * 4 < y.len) return kSearchGlobal;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kSearchGlobal;
   return kStream;
 }
 
@@ -189,7 +189,7 @@ __device__ __forceinline__ uint8_t row_kind_unpruned(const YInfo& y, uint32_t a,
     return (stream < a) ? kStream : kProbe;
   }
   const uint64_t search = (uint64_t)a * (32 - __clz(y.len)) * 4;
-  return (search < stream) ? kSearchGlobal : kStream;
+  return (y.c0 != kNoAlgo && search < stream) ? kSearchGlobal : kStream;
 }
 
 // ---- group-level row bodies: kG lanes, gl = lane within the group --------

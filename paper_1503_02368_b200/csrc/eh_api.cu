@@ -76,7 +76,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
     if (n && (!src || !dst)) eh::fail(EH_EINVAL, "eh_load_edges: NULL src/dst with n = %llu", (unsigned long long)n);
     if ((c.dev_alloc == nullptr) != (c.dev_free == nullptr))
       eh::fail(EH_EINVAL, "eh_load_edges: dev_alloc and dev_free must be set together");
-    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT))
+    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO))
       eh::fail(EH_EINVAL, "eh_load_edges: unknown flags 0x%x", c.flags);
     int ndev = 0;
     EH_CUDA(cudaGetDeviceCount(&ndev));
@@ -91,7 +91,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
     eh_graph* g = new eh_graph();
     try {
       g->device = dev;
-      g->flags = c.flags;
+      g->flags = c.flags | ((c.flags & EH_NO_ALGO) ? EH_ALL_UINT : 0u);  // -RA implies -R
       g->tau = c.bitset_tau ? c.bitset_tau : 128;
       g->min_bitset_card = c.min_bitset_card ? c.min_bitset_card : 2;
       g->bin_small_max = c.bin_small_max;

@@ -6,6 +6,10 @@
 
 namespace eh {
 
+// desc[v].w of every set of an EH_NO_ALGO graph (all uint): row dispatch never
+// chooses the galloping (binary-search) side -- the paper's "-RA" ablation.
+constexpr uint32_t kNoAlgo = 0xFFFFFFFFu;
+
 struct YInfo {
   uint32_t list;  // col offset of N+(y) in 16-B units
   uint32_t len;   // |N+(y)|

@@ -148,7 +148,7 @@ def test_huge_star_and_hub():
 
 
 # ------------------------------------------------------------------ invariances (T5/T6) --
-@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True),
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True),
                                 dict(min_bitset_card=1), dict(bin_small_max=2**32 - 1),
                                 dict(bin_small_max=1, bin_large_min=1), dict(bin_small_max=1, bin_large_min=2**32 - 1),
                                 dict(torch_allocator=True)])
