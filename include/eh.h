@@ -51,6 +51,9 @@ enum {
 #define EH_INPUT_ON_DEVICE 0x1u /* src/dst are device pointers (else host memory, pageable or pinned) */
 #define EH_SET_DEVICE      0x2u /* use cfg->device instead of the current device */
 #define EH_ALL_UINT        0x4u /* relation-level layout, the paper's "-R" ablation: no bitsets */
+#define EH_BLOCK_LAYOUT    0x10u /* NEXT-3 block-level (composite) layout for eh_count_triangles:
+                                    every set is split into 128-id blocks; blocks with >= 4 elements are bitset
+                                    blocks, the rest stay uint (the set-level layouts serve the other queries) */
 #define EH_NO_ALGO         0x8u /* the paper's "-RA" ablation (NEXT-3): EH_ALL_UINT and no
                                    intersection-algorithm choice (every uint cap uint streams, no galloping) */
 
@@ -68,7 +71,7 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* stream, void* ctx);
   void (*dev_free)(void* ptr, void* stream, void* ctx);
   void* alloc_ctx;
-  uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO */
+  uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT */
   /* Count-kernel work classes by d = |N+(x)|: 0 = [2, bin_small_max], 1 = up to
    * bin_large_min - 1, 2 = the rest.  Triangle / per-vertex kernels: class 0 warp-per-x,
    * classes 1-2 CTA-per-x; 4-clique kernels: classes 0-1 warp-per-x, class 2 CTA-per-x.

@@ -234,6 +234,88 @@ __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restri
   return c;
 }
 
+// ---- NEXT-3 block-level (composite) layout (EH_BLOCK_LAYOUT, trie.cu) -------
+struct BlockView {
+  const uint4* bdesc;
+  const uint32_t* bcol;
+  const uint32_t* bcid;
+  const uint4* bmask;
+};
+
+// y's composite set as a YInfo: list/len = its uint (sparse) part, pool = first
+// dense block, c0 = number of dense blocks, c1 = 0 (no set-level bitset).
+__device__ __forceinline__ YInfo yinfo_block(const BlockView& bv, uint32_t y) {
+  const uint4 b = __ldg(bv.bdesc + y);
+  const uint32_t z1 = __ldg(&bv.bdesc[y + 1].z);
+  return YInfo{b.x, b.y, b.z, z1 - b.z, 0u};
+}
+
+// Min property on composite sets: when |A| is small against y, every a in A is
+// looked up (binary search of its block among y's dense blocks, then a bit test
+// or a binary search of the sparse part) -- kProbe; otherwise the sparse part
+// follows the uint rules (kSearchGlobal / kStream) and the dense blocks are
+// ANDed (rows with only dense blocks: kAnd).
+__device__ __forceinline__ uint8_t row_kind_block(const YInfo& y, uint32_t a) {
+  if (a == 0 || (y.len == 0 && y.c0 == 0)) return kSkip;
+  const uint32_t lgs = 32 - __clz(y.len), lgd = 32 - __clz(y.c0);
+  if ((uint64_t)a * (lgs + lgd) * 4 < (uint64_t)y.len + 4ull * y.c0) return kProbe;
+  if (y.len == 0) return kAnd;
+  if ((uint64_t)a * lgs * 4 < y.len) return kSearchGlobal;
+  return kStream;
+}
+
+__device__ __forceinline__ uint32_t block_member(const BlockView& bv, const YInfo& y, uint32_t e) {
+  const uint32_t c = e >> 7;
+  uint32_t lo = 0, len = y.c0;  // lower_bound of c among the dense block numbers
+  const uint32_t* ids = bv.bcid + y.pool;
+  while (len > 0) {
+    const uint32_t h = len >> 1;
+    if (__ldg(ids + lo + h) < c) { lo += h + 1; len -= h + 1; } else { len = h; }
+  }
+  if (lo < y.c0 && __ldg(ids + lo) == c) {
+    const uint4 m = __ldg(bv.bmask + y.pool + lo);
+    const uint32_t q = (e >> 5) & 3, w = q == 0 ? m.x : q == 1 ? m.y : q == 2 ? m.z : m.w;
+    return (w >> (e & 31)) & 1u;
+  }
+  return gmem_search(bv.bcol + (uint64_t)y.list * 4, y.len, e);
+}
+
+// |A cap N+(y)| = |A cap sparse(y)| + |A cap dense(y)|: the sparse part as a uint
+// row, each dense block ANDed with x's staged bitmap chunk (bitset cap bitset,
+// PAPER.md:636) or, when x is hashed, its bits looked up one by one.
+__device__ __forceinline__ uint32_t grp_row_block(uint8_t kd, const BlockView& bv, const uint32_t* __restrict__ bs,
+                                                  const YInfo& y, const XSet& X, const uint32_t* A, uint32_t na,
+                                                  uint32_t gl) {
+  if (kd == kProbe) {
+    uint32_t c = 0;
+    for (uint32_t j = gl; j < na; j += kG) c += block_member(bv, y, A[j]);
+    return c;
+  }
+  uint32_t c = (kd == kStream || kd == kSearchGlobal) ? grp_row(kd, bv.bcol, bs, y, X, A, na, gl) : 0u;
+  const uint32_t nd = y.c0;
+  const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
+  const uint4* xb = reinterpret_cast<const uint4*>(X.tab);
+  for (uint32_t k = gl; k < nd; k += kG) {
+    const uint32_t cc = __ldg(bv.bcid + y.pool + k);
+    const uint4 m = __ldg(bv.bmask + y.pool + k);
+    if (X.mode == kBitmap) {
+      if (cc >= xc0 && cc < xc1) c += and4(m, xb[cc - xc0]);
+    } else {
+      const uint32_t w[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t t = w[q];
+        while (t) {
+          const uint32_t b = __ffs(t) - 1;
+          t &= t - 1;
+          c += X.contains(cc * 128 + q * 32 + b);
+        }
+      }
+    }
+  }
+  return c;
+}
+
 // ------------------------------------------------------------ warp kernel --
 // One warp per x with 2 <= |N+(x)| <= kWarpMaxD.  Lanes classify the rows in
 // parallel, rows are ordered by kind, then the 4 groups take rows round-robin.
@@ -247,12 +329,12 @@ struct __align__(16) WarpSmem {
 
 // kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
 // N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
-template <bool kUnpruned>
+template <bool kUnpruned, bool kBlock>
 __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
                                                              const uint32_t* __restrict__ work, uint64_t nwork,
-                                                             unsigned long long* __restrict__ ctr) {
+                                                             unsigned long long* __restrict__ ctr, BlockView bv) {
   extern __shared__ __align__(16) uint32_t dsm_w[];
   WarpSmem* sm_all = reinterpret_cast<WarpSmem*>(dsm_w);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -276,11 +358,12 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
     const uint32_t nrows = kUnpruned ? d : d - 1;
     bool need_x = false;  // only AND and STREAM rows read x's staged structure
     for (uint32_t i = lane; i < nrows; i += 32) {
-      const YInfo y = yinfo(desc, sm.xs[i]);
-      const uint8_t kd = kUnpruned ? row_kind_unpruned(y, d, X) : row_kind(y, nrows - i, X);
+      const YInfo y = kBlock ? yinfo_block(bv, sm.xs[i]) : yinfo(desc, sm.xs[i]);
+      const uint8_t kd = kBlock ? row_kind_block(y, nrows - i)
+                       : kUnpruned ? row_kind_unpruned(y, d, X) : row_kind(y, nrows - i, X);
       sm.yi[i] = y;
       sm.kind[i] = kd;
-      need_x |= (kd == kAnd || kd == kStream);
+      need_x |= kBlock || (kd == kAnd || kd == kStream);
     }
     if (__any_sync(kFull, need_x)) fill_xset(X, lane, 32);
     __syncwarp();
@@ -299,8 +382,9 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
     __syncwarp();
     for (uint32_t r = grp; r < nr; r += 32 / kG) {
       const uint32_t i = sm.ord[r];
-      cnt += kUnpruned ? grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
-                   : grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
+      cnt += kBlock ? grp_row_block(sm.kind[i], bv, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl)
+           : kUnpruned ? grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
+                       : grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -312,7 +396,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32) k_tri_warp(const uint4* __rest
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
-template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned>  // kXCap > 0: compile-time staging capacity
+template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -320,7 +404,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
                                                             unsigned long long* __restrict__ ctr, uint32_t xcap_rt,
                                                             const unsigned long long* __restrict__ items,
                                                             const uint32_t* __restrict__ hslot,
-                                                            uint32_t* __restrict__ hub_bm, uint32_t hub_words) {
+                                                            uint32_t* __restrict__ hub_bm, uint32_t hub_words,
+                                                            BlockView bv) {
   // kUnpruned: work items are (x << 32 | first row) over row ranges of kRowsPerItem
   // (hub lists of the symmetric trie would otherwise leave one CTA with 10^5 rows)
   const uint32_t xcap = kXCap > 0 ? (uint32_t)kXCap : xcap_rt;
@@ -374,13 +459,18 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_tri_cta(const uint4* __restr
     __syncthreads();
     const uint32_t nrows = kUnpruned ? min(d, r0 + kRowsPerItem) : d - 1;
     uint32_t i = r0 + gid;
-    YInfo y = (i < nrows) ? yinfo(desc, xs[i]) : YInfo{0, 0, 0, 0, 0};
+    YInfo y = (i < nrows) ? (kBlock ? yinfo_block(bv, xs[i]) : yinfo(desc, xs[i])) : YInfo{0, 0, 0, 0, 0};
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
-      const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
+      const YInfo ynext = (inext < nrows) ? (kBlock ? yinfo_block(bv, xs[inext]) : yinfo(desc, xs[inext]))
+                                          : YInfo{0, 0, 0, 0, 0};
       const uint32_t na = kUnpruned ? d : nrows - i;
-      const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind(y, na, X);
-      cnt += grp_row(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+      if (kBlock) {
+        cnt += grp_row_block(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
+      } else {
+        const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind(y, na, X);
+        cnt += grp_row(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+      }
       i = inext;
       y = ynext;
     }
@@ -430,10 +520,10 @@ __global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __res
   }
 }
 
-template <int NW, int TABW, int XCAP, bool kUnpruned>
+template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
-  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned>;
+  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> items;
@@ -479,13 +569,14 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>(nitems, (uint64_t)kSMs * std::max(1, per_sm));
   k<<<grid, NW * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nitems, g->d_counter, xcap, items.p,
-                                kUnpruned ? hslot.p : nullptr, hub_bm.p, hub_words);
+                                kUnpruned ? hslot.p : nullptr, hub_bm.p, hub_words,
+                                BlockView{g->bdesc, g->bcol, g->bcid, g->bmask});
   EH_LAUNCH("k_tri_cta");
   if (kUnpruned) EH_CUDA(cudaStreamSynchronize(s));  // items is released on return
 }
 
 
-template <bool kUnpruned>
+template <bool kUnpruned, bool kBlock>
 uint64_t count_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
@@ -499,15 +590,18 @@ uint64_t count_impl(eh_graph* g) {
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
     uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
-    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned>(g, nsmall, nlarge, 0);
-    else if (wide) launch_cta<16, 16384, 0, kUnpruned>(g, nsmall, nlarge, xcap);
-    else launch_cta<4, 2048, 0, kUnpruned>(g, nsmall, nlarge, xcap);
+    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock>(g, nsmall, nlarge, 0);
+    else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
+    else launch_cta<4, 2048, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(WarpSmem) * kWK_Warps;
-    EH_CUDA(cudaFuncSetAttribute(k_tri_warp<kUnpruned>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_tri_warp<kUnpruned><<<grid, kWK_Warps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    EH_CUDA(cudaFuncSetAttribute(k_tri_warp<kUnpruned, kBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_tri_warp<kUnpruned, kBlock><<<grid, kWK_Warps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall,
+                                                                      g->d_counter,
+                                                                      BlockView{g->bdesc, g->bcol, g->bcid, g->bmask});
     EH_LAUNCH("k_tri_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -517,10 +611,12 @@ uint64_t count_impl(eh_graph* g) {
 
 }  // namespace
 
-uint64_t count_triangles(eh_graph* g) { return count_impl<false>(g); }
+uint64_t count_triangles(eh_graph* g) {
+  return g->bdesc ? count_impl<false, true>(g) : count_impl<false, false>(g);  // NEXT-3 block layout if built
+}
 
 // NEXT-2: the unpruned nest over the symmetric trie (built on first use) = 6T.
-uint64_t count_triangles_unpruned(eh_graph* g) { return count_impl<true>(symmetric_trie(g)); }
+uint64_t count_triangles_unpruned(eh_graph* g) { return count_impl<true, false>(symmetric_trie(g)); }
 
 uint32_t tri_warp_max_degree() { return kWarpMaxD; }
 

@@ -76,7 +76,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
     if (n && (!src || !dst)) eh::fail(EH_EINVAL, "eh_load_edges: NULL src/dst with n = %llu", (unsigned long long)n);
     if ((c.dev_alloc == nullptr) != (c.dev_free == nullptr))
       eh::fail(EH_EINVAL, "eh_load_edges: dev_alloc and dev_free must be set together");
-    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO))
+    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT))
       eh::fail(EH_EINVAL, "eh_load_edges: unknown flags 0x%x", c.flags);
     int ndev = 0;
     EH_CUDA(cudaGetDeviceCount(&ndev));
@@ -132,6 +132,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       eh::build_trie(g, d_src, d_dst, n, &timer);
       in.reset();
       eh::build_layouts(g);
+      if (g->flags & EH_BLOCK_LAYOUT) eh::build_block_layout(g);
       timer.mark("layouts");
       eh::build_worklists(g);
       timer.mark("worklists");

@@ -207,6 +207,14 @@ struct eh_graph {
   uint32_t* orig_id = nullptr;  // original id of each rank
   uint32_t* deg_rank = nullptr; // degree (distinct neighbours) of each rank
   uint32_t* bytes32 = nullptr;  // bytes(N+(v)) at tau = 32 (B_tri accounting)
+  // NEXT-3 block-level (composite) layout, built with EH_BLOCK_LAYOUT (trie.cu):
+  // bdesc[v] = {sparse list offset (16-B units in bcol), #sparse elements, first dense
+  // block (prefix into bcid / bmask), 0}; #dense blocks = bdesc[v+1].z - bdesc[v].z.
+  uint4* bdesc = nullptr;
+  uint32_t* bcol = nullptr;     // sparse elements, padded per list to 16 B
+  uint32_t* bcid = nullptr;     // dense 128-id block numbers (absolute), ascending per set
+  uint4* bmask = nullptr;       // their 128-bit masks
+  uint64_t n_dense_blocks = 0, n_sparse_elems = 0;
   bool stats_ready = false;
   // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
   uint32_t* work = nullptr;
@@ -232,6 +240,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
 // trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
 void build_layouts(eh_graph* g);
 void compute_stats(eh_graph* g);  // lazy: B_tri, wedge work, #bitset sets
+void build_block_layout(eh_graph* g);  // NEXT-3 composite layout (EH_BLOCK_LAYOUT)
 void build_worklists(eh_graph* g);
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);

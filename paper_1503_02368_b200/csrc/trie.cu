@@ -141,6 +141,64 @@ void build_layouts(eh_graph* g) {
   }
 }
 
+// ---- NEXT-3: block-level (composite) layout -------------
+// Each set N+(v) is split into 128-id blocks (the chunks of the set-level
+// bitsets, reading c11); a block holding >= kDenseMin elements becomes a bitset
+// block (16 B <= 4 B per element, the set optimizer's space rule applied per
+// block), the others stay uint.  One thread per set, two passes (count, fill).
+constexpr uint32_t kDenseMin = 4;
+
+__global__ void k_block_count(const uint4* __restrict__ desc, const uint32_t* __restrict__ col, uint64_t n,
+                              uint32_t* __restrict__ ns4, uint32_t* __restrict__ nd) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 d = desc[v];
+    const uint32_t* l = col + (uint64_t)d.x * 4;
+    uint32_t sparse = 0, dense = 0;
+    for (uint32_t i = 0; i < d.y;) {
+      const uint32_t c = l[i] >> 7;
+      uint32_t j = i + 1;
+      while (j < d.y && (l[j] >> 7) == c) ++j;
+      if (j - i >= kDenseMin) ++dense; else sparse += j - i;
+      i = j;
+    }
+    ns4[v] = (sparse + 3) >> 2;
+    nd[v] = dense;
+  }
+}
+
+__global__ void k_block_fill(const uint4* __restrict__ desc, const uint32_t* __restrict__ col, uint64_t n,
+                             const uint64_t* __restrict__ soff16, const uint64_t* __restrict__ doff,
+                             uint32_t* __restrict__ bcol, uint32_t* __restrict__ bcid, uint4* __restrict__ bmask,
+                             uint4* __restrict__ bdesc, uint64_t total16, uint64_t total_dense) {
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += (uint64_t)gridDim.x * blockDim.x) {
+    if (v == n) {
+      bdesc[n] = make_uint4((uint32_t)total16, 0u, (uint32_t)total_dense, 0u);
+      continue;
+    }
+    const uint4 d = desc[v];
+    const uint32_t* l = col + (uint64_t)d.x * 4;
+    uint32_t* sp = bcol + soff16[v] * 4;
+    uint64_t db = doff[v];
+    uint32_t ns = 0;
+    for (uint32_t i = 0; i < d.y;) {
+      const uint32_t c = l[i] >> 7;
+      uint32_t j = i + 1;
+      while (j < d.y && (l[j] >> 7) == c) ++j;
+      if (j - i >= kDenseMin) {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        for (uint32_t k = i; k < j; ++k) w[(l[k] >> 5) & 3] |= 1u << (l[k] & 31);
+        bcid[db] = c;
+        bmask[db] = make_uint4(w[0], w[1], w[2], w[3]);
+        ++db;
+      } else {
+        for (uint32_t k = i; k < j; ++k) sp[ns++] = l[k];
+      }
+      i = j;
+    }
+    bdesc[v] = make_uint4((uint32_t)soff16[v], ns, (uint32_t)doff[v], 0u);
+  }
+}
+
 // Statistics that are not needed by the counts (B_tri, wedge work, number of
 // bitset sets) are computed on the first eh_graph_stats call, off the load path.
 void compute_stats(eh_graph* g) {
@@ -163,6 +221,35 @@ void compute_stats(eh_graph* g) {
     g->alg_bytes_tri = 8;
   }
   g->stats_ready = true;
+}
+
+void build_block_layout(eh_graph* g) {
+  Allocator& al = g->alloc;
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n_act;
+  const unsigned TB = 256;
+  DBuf<uint32_t> ns4(al, std::max<uint64_t>(1, n)), nd(al, std::max<uint64_t>(1, n));
+  if (n) {
+    k_block_count<<<grid_for(n, TB), TB, 0, s>>>(g->desc, g->col, n, ns4.p, nd.p);
+    EH_LAUNCH("k_block_count");
+  }
+  DBuf<uint64_t> soff(al, n + 1), doff(al, n + 1), tot(al, 2);
+  scan_exclusive_u32(ns4.p, soff.p, n, tot.p, al, s);
+  scan_exclusive_u32(nd.p, doff.p, n, tot.p + 1, al, s);
+  uint64_t h[2] = {0, 0};
+  EH_CUDA(cudaMemcpyAsync(h, tot.p, 16, cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  if (h[0] >= (1ull << 32) || h[1] >= (1ull << 32)) fail(EH_EINVAL, "block layout too large");
+  g->bcol = (uint32_t*)g->own(std::max<uint64_t>(16, h[0] * 16));
+  EH_CUDA(cudaMemsetAsync(g->bcol, 0xFF, std::max<uint64_t>(16, h[0] * 16), s));
+  g->bcid = (uint32_t*)g->own(std::max<uint64_t>(1, h[1]) * 4);
+  g->bmask = (uint4*)g->own(std::max<uint64_t>(1, h[1]) * 16);
+  g->bdesc = (uint4*)g->own((n + 1) * sizeof(uint4));
+  k_block_fill<<<grid_for(n + 1, TB), TB, 0, s>>>(g->desc, g->col, n, soff.p, doff.p, g->bcol, g->bcid, g->bmask,
+                                                  g->bdesc, h[0], h[1]);
+  EH_LAUNCH("k_block_fill");
+  g->n_dense_blocks = h[1];
+  EH_CUDA(cudaStreamSynchronize(s));
 }
 
 void build_worklists(eh_graph* g) {

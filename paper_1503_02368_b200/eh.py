@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libeh.so")
 
 EH_OK, EH_EINVAL, EH_ENOMEM, EH_ECUDA, EH_EUNSORTED = 0, -1, -2, -3, -4
 EH_COUNT_ERROR = 2**64 - 1
-EH_INPUT_ON_DEVICE, EH_SET_DEVICE, EH_ALL_UINT, EH_NO_ALGO = 0x1, 0x2, 0x4, 0x8
+EH_INPUT_ON_DEVICE, EH_SET_DEVICE, EH_ALL_UINT, EH_NO_ALGO, EH_BLOCK_LAYOUT = 0x1, 0x2, 0x4, 0x8, 0x10
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -162,7 +162,8 @@ class Stats:
 class Graph:
     """A loaded trie (eh_graph*).  ``Graph(src, dst, ...)`` == eh_load_edges_ex."""
 
-    def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False, bin_small_max: int = 0,
+    def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False,
+                 block_layout: bool = False, bin_small_max: int = 0,
                  bin_large_min: int = 0, min_bitset_card: int = 0, stream=None, device: int | None = None,
                  torch_allocator: bool = False):
         L = lib()
@@ -175,7 +176,8 @@ class Graph:
             raise ValueError("src and dst must both be host or both be device memory")
         cfg = EHConfig()
         cfg.bitset_tau = tau
-        cfg.flags = (EH_INPUT_ON_DEVICE if sdev else 0) | (EH_ALL_UINT if all_uint else 0) | (EH_NO_ALGO if no_algo else 0)
+        cfg.flags = (EH_INPUT_ON_DEVICE if sdev else 0) | (EH_ALL_UINT if all_uint else 0) | (EH_NO_ALGO if no_algo else 0) \
+            | (EH_BLOCK_LAYOUT if block_layout else 0)
         if device is not None:
             cfg.flags |= EH_SET_DEVICE
             cfg.device = device

@@ -148,7 +148,8 @@ def test_huge_star_and_hub():
 
 
 # ------------------------------------------------------------------ invariances (T5/T6) --
-@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True),
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(block_layout=True),
+                                dict(block_layout=True, tau=2), dict(block_layout=True, bin_large_min=1),
                                 dict(min_bitset_card=1), dict(bin_small_max=2**32 - 1),
                                 dict(bin_small_max=1, bin_large_min=1), dict(bin_small_max=1, bin_large_min=2**32 - 1),
                                 dict(torch_allocator=True)])
@@ -298,3 +299,31 @@ def test_repeated_counts_and_many_handles():
     assert first == again
     for g in graphs:
         g.close()
+
+
+# ------------------------------------------------- NEXT-3 block-level layout --
+@pytest.mark.parametrize("seed", range(8))
+def test_block_layout_vs_oracle(seed):
+    """EH_BLOCK_LAYOUT: composite sets (128-id blocks, bitset blocks when >= 4
+    elements) for the triangle count -- same counts as the oracle."""
+    rng = np.random.default_rng(900 + seed)
+    if seed % 3 == 0:
+        src, dst = synth.rmat(int(rng.integers(8, 15)), 16, 900 + seed)
+    elif seed % 3 == 1:
+        src, dst = synth.er(int(rng.integers(50, 800)), float(rng.choice([0.05, 0.3, 0.8])), 900 + seed)
+    else:
+        src, dst = synth.complete_multipartite(tuple(int(x) for x in rng.integers(1, 60, size=4)))
+    t, k, _ = _gpu_counts(src, dst, k4=True, block_layout=True)
+    assert t == oracle.count_triangles(src, dst)
+    assert k == oracle.count_4cliques(src, dst)  # other queries keep the set-level layouts
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(bin_small_max=2**32 - 1), dict(bin_large_min=1)])
+def test_block_layout_dense_and_hashed_x(kw, monkeypatch):
+    # K_400: every block dense; EH_TRI_XCAP forces hashed / sorted x structures (bit-by-bit dense path)
+    from math import comb
+    assert _gpu_counts(*synth.complete(400), k4=False, block_layout=True, **kw)[0] == comb(400, 3)
+    monkeypatch.setenv("EH_TRI_XCAP", "128")
+    assert _gpu_counts(*synth.complete(400), k4=False, block_layout=True, **kw)[0] == comb(400, 3)
+    src, dst = synth.rmat(12, 16, 4)
+    assert _gpu_counts(src, dst, k4=False, block_layout=True, **kw)[0] == oracle.count_triangles(src, dst)

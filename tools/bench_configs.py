@@ -19,6 +19,7 @@ PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
     os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6538.6
 NEXT1 = "--next1" in sys.argv
 NEXT2 = "--next2" in sys.argv
+NEXT3 = "--next3" in sys.argv
 names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"]
 reps = 5
 for name in names:
@@ -121,6 +122,33 @@ for name in names:
                         f"unpruned{label}_gbs": sst.alg_bytes_tri / um / 1e6,
                         f"unpruned{label}_frac": sst.alg_bytes_tri / um / 1e6 / PEAK,
                         f"sym_bitset_sets{label}": sst.n_bitset_sets, f"sym_max_degree": sst.max_out_degree})
+    if NEXT3:  # relation / set / block level layouts, -R and -RA ablations
+        for label, kw in (("set", {}), ("R", {"all_uint": True}), ("RA", {"no_algo": True}),
+                          ("block", {"block_layout": True})):
+            with torch.cuda.stream(st):
+                ts, lt, ks, ls = [], [], [], []
+                for r in range(reps):
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                    ev[0].record(st)
+                    g = eh.Graph(s, d, stream=st, **kw)
+                    ev[1].record(st)
+                    tv = g.count_triangles()
+                    ev[2].record(st)
+                    kv = g.count_4cliques() if cfg.query == "4cliques" and label != "block" else None
+                    ev[3].record(st)
+                    lv = g.count_lollipop() if label != "block" else None
+                    ev[4].record(st)
+                    st.synchronize()
+                    g.close()
+                    lt.append(ev[0].elapsed_time(ev[1]))
+                    ts.append(ev[1].elapsed_time(ev[2]))
+                    ks.append(ev[2].elapsed_time(ev[3]))
+                    ls.append(ev[3].elapsed_time(ev[4]))
+                assert tv == res["triangles"], (label, tv)
+                res[f"layout_{label}"] = {"load_ms": statistics.median(lt), "tri_ms": statistics.median(ts),
+                                          "k4_ms": statistics.median(ks) if kv is not None else None,
+                                          "k4": kv, "lollipop_ms": statistics.median(ls) if lv is not None else None,
+                                          "lollipop": str(lv) if lv is not None else None}
     print(json.dumps(res), flush=True)
     del s, d
     torch.cuda.empty_cache()
