@@ -81,7 +81,23 @@ typedef struct {
   uint32_t bin_small_max;
   uint32_t bin_large_min;
   uint32_t min_bitset_card;/* bitset only if |S| >= this (reading c15); 0 -> 2 */
+  /* NEXT-4 node ordering = the id assignment that orients (prunes) the edges
+   * (PAPER.md:1065-1153); counts never depend on it.  EH_ORDER_* below;
+   * 0 = EH_ORDER_DEGREE, the paper's default. */
+  uint32_t order;
 } eh_config;
+
+/* Node orderings (readings in DESIGN.md c20).  Each names the
+ * paper's labelling; edges are kept from the later to the earlier label (the
+ * mirror of "src_id > dst_id"). */
+enum {
+  EH_ORDER_DEGREE = 0,     /* descending degree (ties by id) -- the default */
+  EH_ORDER_REV_DEGREE = 1, /* ascending degree */
+  EH_ORDER_RANDOM = 2,     /* a fixed pseudo-random permutation of the ids */
+  EH_ORDER_BFS = 3,        /* breadth-first from the highest-degree vertex (level, then id) */
+  EH_ORDER_HYBRID = 4,     /* BFS labels, then stably sorted by descending degree */
+  EH_ORDER_SHINGLE = 5     /* by neighbourhood min-hash (shingle), then id */
+};
 
 /* eh_stats: filled by eh_graph_stats (bench / tests). */
 typedef struct {

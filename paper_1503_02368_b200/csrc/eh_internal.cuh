@@ -193,6 +193,7 @@ struct eh_graph {
   eh::Allocator alloc;
   uint32_t flags = 0, tau = 32, min_bitset_card = 2;
   uint32_t bin_small_max = 0, bin_large_min = 0;
+  uint32_t order = 0;  // NEXT-4: EH_ORDER_*
 
   uint64_t n_input = 0, m = 0, n_act = 0, max_dplus = 0;
   uint64_t n_bitsets = 0, bs_words = 0, col_elems = 0;

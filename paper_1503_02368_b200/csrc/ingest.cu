@@ -143,23 +143,104 @@ struct ActivePred {
   const uint32_t* deg;
   __device__ bool operator()(uint64_t i) const { return deg[i] != 0; }
 };
-struct RankKeyEmit {  // (deg << b) | id, sorted ascending = the (degree, id) order
+struct RankKeyEmit {  // (primary << b) | id, sorted ascending = the rank order (primary = deg by default)
+  const uint64_t* prim;  // nullptr: primary = deg
   const uint32_t* deg;
   uint32_t b;
   uint64_t* out;
-  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = ((uint64_t)deg[i] << b) | i; }
+  __device__ void operator()(uint64_t pos, uint64_t i) const {
+    out[pos] = ((prim ? prim[i] : (uint64_t)deg[i]) << b) | i;
+  }
 };
 
-__global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint32_t b, uint32_t* __restrict__ rank,
+__global__ void k_rank(const uint64_t* __restrict__ sorted, uint64_t n_act, uint32_t b, uint32_t* __restrict__ deg_rank_id,
                        uint32_t* __restrict__ orig, const uint32_t* __restrict__ dict, uint32_t* __restrict__ deg_rank) {
+  // deg_rank_id holds deg[id] on entry and rank[id] on exit (one thread per id: read, then write)
   const uint64_t mask = (1ull << b) - 1ull;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_act; r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t key = sorted[r];
     const uint32_t id = (uint32_t)(key & mask);
-    rank[id] = (uint32_t)r;
+    deg_rank[r] = deg_rank_id[id];
+    deg_rank_id[id] = (uint32_t)r;
     orig[r] = dict ? dict[id] : id;
-    deg_rank[r] = (uint32_t)(key >> b);  // the key is (deg << b) | id
   }
+}
+
+// ---- NEXT-4 node orderings (reading c20) ------
+// Each ordering gives every id a primary key; ranks ascend by (primary, id) and
+// edges point low -> high rank, the mirror of the paper's labels with
+// "src_id > dst_id", so primary = the REVERSE of the paper's label order.
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {  // splitmix-style finaliser
+  x ^= 0x9E3779B9u;
+  x ^= x >> 16; x *= 0x7FEB352Du;
+  x ^= x >> 15; x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__global__ void k_prim_simple(const uint32_t* __restrict__ deg, uint64_t n, uint32_t order, uint32_t max_deg,
+                              const uint32_t* __restrict__ aux, uint32_t aux_max, uint32_t aux_bits,
+                              uint64_t* __restrict__ prim) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t p = 0;
+    if (order == EH_ORDER_REV_DEGREE) p = max_deg - deg[i];
+    else if (order == EH_ORDER_RANDOM) p = hash32((uint32_t)i);
+    else if (order == EH_ORDER_SHINGLE) p = 0xFFFFFFFFu - aux[i];  // aux = min-hash of N(i)
+    else if (order == EH_ORDER_BFS) p = aux_max - aux[i];           // aux = BFS level (aux_max: unreached)
+    else if (order == EH_ORDER_HYBRID) p = ((uint64_t)deg[i] << aux_bits) | (aux_max - aux[i]);
+    prim[i] = p;
+  }
+}
+
+__global__ void k_shingle(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint32_t* __restrict__ sh) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(keys[i] >> b), v = (uint32_t)(keys[i] & mask);
+    atomicMin(&sh[u], hash32(v));
+    atomicMin(&sh[v], hash32(u));
+  }
+}
+
+// undirected adjacency by id for the BFS orderings
+__global__ void k_adj_fill(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint64_t* __restrict__ off,
+                           uint32_t* __restrict__ cur, uint32_t* __restrict__ adj) {
+  const uint64_t mask = (1ull << b) - 1ull;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(keys[i] >> b), v = (uint32_t)(keys[i] & mask);
+    adj[off[u] + atomicAdd(&cur[u], 1u)] = v;
+    adj[off[v] + atomicAdd(&cur[v], 1u)] = u;
+  }
+}
+
+__global__ void k_bfs_root(const uint32_t* __restrict__ deg, uint64_t n, unsigned long long* __restrict__ best) {
+  unsigned long long b = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    b = max(b, ((unsigned long long)deg[i] << 32) | (0xFFFFFFFFull - i));  // max degree, then smallest id
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(kFull, b, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(best, b);
+}
+
+// one level: warp per frontier vertex, lanes over its neighbours
+__global__ void k_bfs_step(const uint32_t* __restrict__ frontier, uint32_t nf, const uint64_t* __restrict__ off,
+                           const uint32_t* __restrict__ adj, uint32_t* __restrict__ level, uint32_t next_level,
+                           uint32_t* __restrict__ next, uint32_t* __restrict__ nnext) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = warp; k < nf; k += nw) {
+    const uint32_t v = frontier[k];
+    for (uint64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+      const uint32_t u = adj[e];
+      if (level[u] == 0xFFFFFFFFu && atomicCAS(&level[u], 0xFFFFFFFFu, next_level) == 0xFFFFFFFFu)
+        next[atomicAdd(nnext, 1u)] = u;
+    }
+  }
+}
+
+__global__ void k_level_fix(uint32_t* __restrict__ level, uint64_t n, uint32_t unreached) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (level[i] == 0xFFFFFFFFu) level[i] = unreached;
 }
 
 // a5: orient low rank -> high rank: out-degree histogram of the low end.
@@ -234,6 +315,45 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* 
 }
 
 }  // namespace
+
+// BFS levels from the highest-degree id over the undirected simple graph of the
+// distinct keys; ids not reached get the returned value (max level + 1).
+static uint32_t bfs_levels(const uint64_t* keys, uint64_t m, uint32_t b, const uint32_t* deg, uint64_t n_ids,
+                           uint32_t* level, Allocator& al, cudaStream_t s) {
+  const unsigned TB = 256;
+  DBuf<uint64_t> off(al, n_ids + 1), tot(al, 1);
+  scan_exclusive_u32(deg, off.p, n_ids, tot.p, al, s);
+  EH_CUDA(cudaMemcpyAsync(off.p + n_ids, tot.p, 8, cudaMemcpyDeviceToDevice, s));  // off[n] = 2m
+  DBuf<uint32_t> cur(al, n_ids), adj(al, std::max<uint64_t>(1, 2 * m)), fa(al, n_ids), fb(al, n_ids), cnt(al, 1);
+  EH_CUDA(cudaMemsetAsync(cur.p, 0, n_ids * 4, s));
+  k_adj_fill<<<grid_for(m, TB * 4), TB, 0, s>>>(keys, m, b, off.p, cur.p, adj.p);
+  EH_LAUNCH("k_adj_fill");
+  DBuf<unsigned long long> best(al, 1);
+  EH_CUDA(cudaMemsetAsync(best.p, 0, 8, s));
+  k_bfs_root<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg, n_ids, best.p);
+  EH_LAUNCH("k_bfs_root");
+  const uint32_t root = (uint32_t)(0xFFFFFFFFull - (read_scalar(best.p, s) & 0xFFFFFFFFull));
+  EH_CUDA(cudaMemsetAsync(level, 0xFF, n_ids * 4, s));
+  const uint32_t zero = 0;
+  EH_CUDA(cudaMemcpyAsync(level + root, &zero, 4, cudaMemcpyHostToDevice, s));
+  EH_CUDA(cudaMemcpyAsync(fa.p, &root, 4, cudaMemcpyHostToDevice, s));
+  uint32_t nf = 1, l = 0;
+  uint32_t* f = fa.p;
+  uint32_t* nx = fb.p;
+  while (nf) {
+    EH_CUDA(cudaMemsetAsync(cnt.p, 0, 4, s));
+    k_bfs_step<<<grid_for((uint64_t)nf * 32, TB), TB, 0, s>>>(f, nf, off.p, adj.p, level, l + 1, nx, cnt.p);
+    EH_LAUNCH("k_bfs_step");
+    nf = read_scalar(cnt.p, s);
+    std::swap(f, nx);
+    ++l;
+  }
+  const uint32_t unreached = l;  // levels used: 0 .. l-1
+  // ids never reached (other components, isolated ids) get `unreached`
+  k_level_fix<<<grid_for(n_ids, TB * 4), TB, 0, s>>>(level, n_ids, unreached);
+  EH_LAUNCH("k_level_fix");
+  return unreached;
+}
 
 void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, PhaseTimer* tm) {
   auto mark = [&](const char* p) { if (tm) tm->mark(p); };
@@ -329,13 +449,39 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   k_max_u32<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, dmaxdeg.p);
   EH_LAUNCH("k_max_u32");
   const uint32_t max_deg = read_scalar(dmaxdeg.p, s);
-  // rank keys go into the (free) sorted-key buffer `sk`; need n_act <= n (true: n_act <= 2m <= 2n... use own buffer)
+  // NEXT-4: the primary rank key of the chosen node ordering (default: degree)
+  DBuf<uint64_t> prim;
+  uint32_t pbits = bitlen(max_deg);
+  if (g->order != EH_ORDER_DEGREE && m) {
+    prim = DBuf<uint64_t>(al, n_ids);
+    DBuf<uint32_t> aux;
+    uint32_t aux_max = 0, aux_bits = 0;
+    if (g->order == EH_ORDER_SHINGLE) {
+      aux = DBuf<uint32_t>(al, n_ids);
+      EH_CUDA(cudaMemsetAsync(aux.p, 0xFF, n_ids * 4, s));
+      k_shingle<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, aux.p);
+      EH_LAUNCH("k_shingle");
+      pbits = 32;
+    } else if (g->order == EH_ORDER_BFS || g->order == EH_ORDER_HYBRID) {
+      aux = DBuf<uint32_t>(al, n_ids);
+      aux_max = bfs_levels(ukeys, m, b, deg.p, n_ids, aux.p, al, s);  // aux_max = level of unreached ids
+      aux_bits = bitlen(aux_max);
+      pbits = (g->order == EH_ORDER_BFS) ? aux_bits : bitlen(max_deg) + aux_bits;
+    } else if (g->order == EH_ORDER_RANDOM) {
+      pbits = 32;
+    }
+    if (b + pbits > 64) fail(EH_EINVAL, "node ordering key needs %u bits", b + pbits);
+    k_prim_simple<<<grid_for(n_ids, TB * 4), TB, 0, s>>>(deg.p, n_ids, g->order, max_deg, aux.p, aux_max, aux_bits,
+                                                         prim.p);
+    EH_LAUNCH("k_prim_simple");
+  }
   DBuf<uint64_t> rkeys(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m))),
       ralt(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m)));
-  const uint64_t n_act = select_if(n_ids, ActivePred{deg.p}, RankKeyEmit{deg.p, b, rkeys.p}, al, s);
+  const uint64_t n_act = select_if(n_ids, ActivePred{deg.p}, RankKeyEmit{prim.p, deg.p, b, rkeys.p}, al, s);
   g->n_act = n_act;
-  uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + bitlen(max_deg), al, s);
-  DBuf<uint32_t>& rank = deg;  // reuse: the degree of every active id is already encoded in rkeys
+  uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + pbits, al, s);
+  prim.reset();
+  DBuf<uint32_t>& rank = deg;  // k_rank turns deg[id] into rank[id] (and records deg per rank)
   g->orig_id = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);
   g->deg_rank = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);
   if (n_act) {

@@ -32,7 +32,9 @@ class EHConfig(ctypes.Structure):
     _fields_ = [("bitset_tau", ctypes.c_uint32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", _ALLOC_FN), ("dev_free", _FREE_FN), ("alloc_ctx", ctypes.c_void_p),
                 ("flags", ctypes.c_uint32), ("bin_small_max", ctypes.c_uint32), ("bin_large_min", ctypes.c_uint32),
-                ("min_bitset_card", ctypes.c_uint32)]
+                ("min_bitset_card", ctypes.c_uint32), ("order", ctypes.c_uint32)]
+
+ORDERS = {"degree": 0, "rev_degree": 1, "random": 2, "bfs": 3, "hybrid": 4, "shingle": 5}
 
 
 class EHStats(ctypes.Structure):
@@ -163,7 +165,7 @@ class Graph:
     """A loaded trie (eh_graph*).  ``Graph(src, dst, ...)`` == eh_load_edges_ex."""
 
     def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False,
-                 block_layout: bool = False, bin_small_max: int = 0,
+                 block_layout: bool = False, order: str = "degree", bin_small_max: int = 0,
                  bin_large_min: int = 0, min_bitset_card: int = 0, stream=None, device: int | None = None,
                  torch_allocator: bool = False):
         L = lib()
@@ -184,6 +186,7 @@ class Graph:
         cfg.bin_small_max = bin_small_max
         cfg.bin_large_min = bin_large_min
         cfg.min_bitset_card = min_bitset_card
+        cfg.order = ORDERS[order]
         if stream is not None:
             cfg.stream = getattr(stream, "cuda_stream", stream)
         self._alloc = None
