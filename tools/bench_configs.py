@@ -20,6 +20,7 @@ PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
 NEXT1 = "--next1" in sys.argv
 NEXT2 = "--next2" in sys.argv
 NEXT3 = "--next3" in sys.argv
+NEXT4 = "--next4" in sys.argv
 names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"]
 reps = 5
 for name in names:
@@ -149,6 +150,27 @@ for name in names:
                                           "k4_ms": statistics.median(ks) if kv is not None else None,
                                           "k4": kv, "lollipop_ms": statistics.median(ls) if lv is not None else None,
                                           "lollipop": str(lv) if lv is not None else None}
+    if NEXT4:  # node orderings
+        for order in ("degree", "random", "bfs", "hybrid", "shingle", "rev_degree"):
+            row = {}
+            for label, kw in (("", {}), ("_R", {"all_uint": True})):
+                with torch.cuda.stream(st):
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    ev[0].record(st)
+                    g = eh.Graph(s, d, stream=st, order=order, **kw)
+                    ev[1].record(st)
+                    tv = g.count_triangles()
+                    ev[2].record(st)
+                    uv = g.count_triangles_unpruned() if name != "C5" else None
+                    ev[3].record(st)
+                    st.synchronize()
+                    mo = g.stats().max_out_degree
+                    g.close()
+                assert tv == res["triangles"] and (uv is None or uv == 6 * tv), (order, tv, uv)
+                row.update({f"load{label}_ms": ev[0].elapsed_time(ev[1]), f"pruned{label}_ms": ev[1].elapsed_time(ev[2]),
+                            f"unpruned{label}_ms": ev[2].elapsed_time(ev[3]) if uv is not None else None,
+                            "max_out_degree": mo})
+            res[f"order_{order}"] = row
     print(json.dumps(res), flush=True)
     del s, d
     torch.cuda.empty_cache()
