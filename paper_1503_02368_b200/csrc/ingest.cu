@@ -91,16 +91,6 @@ struct CopySlotEmit {
   __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = t[i]; }
 };
 
-struct UniqueKeyPred {  // a3: first of a run of equal keys, sentinel excluded
-  const uint64_t* k;
-  uint64_t sentinel;
-  __device__ bool operator()(uint64_t i) const { return k[i] != sentinel && (i == 0 || k[i] != k[i - 1]); }
-};
-struct CopyKeyEmit {
-  const uint64_t* k;
-  uint64_t* out;
-  __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = k[i]; }
-};
 struct UniqueU32Pred {
   const uint32_t* k;
   __device__ bool operator()(uint64_t i) const { return i == 0 || k[i] != k[i - 1]; }
@@ -111,32 +101,41 @@ struct CopyU32Emit {
   __device__ void operator()(uint64_t pos, uint64_t i) const { out[pos] = k[i]; }
 };
 
+// The sorted key array is consumed in place (no compaction): an entry counts
+// iff it is the first of its run of equal keys and not the self-loop sentinel
+// (all ones, sorted last).  The hash path's keys are distinct, so the same
+// test accepts all of them.
+__device__ __forceinline__ bool key_head(const uint64_t* __restrict__ keys, uint64_t i, uint64_t sentinel,
+                                         uint64_t& k) {
+  k = keys[i];
+  return k != sentinel && (i == 0 || keys[i - 1] != k);
+}
+
 // a4: degree = number of distinct neighbours.
 // Keys are sorted by the low end u, so u-side counts are run lengths inside a
 // warp (one atomic per run); v-side atomics are aggregated over equal v in the
 // warp (hubs would otherwise serialise thousands of atomics on one address).
-__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint32_t* __restrict__ deg) {
+__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t nk, uint32_t b, uint64_t sentinel,
+                         uint32_t* __restrict__ deg, unsigned long long* __restrict__ m_out) {
   const uint64_t mask = (1ull << b) - 1ull;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
+  uint32_t heads = 0;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < nk; base += stride) {
     const uint64_t i = base + lane;
-    const bool valid = i < m;
-    const uint64_t k = valid ? keys[i] : 0ull;
+    uint64_t k = 0;
+    const bool valid = i < nk && key_head(keys, i, sentinel, k);
+    heads += valid;
     const uint32_t u = valid ? (uint32_t)(k >> b) : 0xFFFFFFFFu;
     const uint32_t v = valid ? (uint32_t)(k & mask) : 0xFFFFFFFFu;
-    const uint32_t uprev = __shfl_up_sync(kFull, u, 1);
-    const bool head = valid && (lane == 0 || u != uprev);
-    const unsigned hm = __ballot_sync(kFull, head), vm = __ballot_sync(kFull, valid);
-    if (head) {
-      const unsigned after = hm & ~((2u << lane) - 1u);
-      const int end = after ? __ffs(after) - 1 : 32 - __clz(vm);
-      atomicAdd(&deg[u], (uint32_t)(end - lane));
-    }
-    const unsigned peers = __match_any_sync(kFull, v);
-    if (valid && (peers & lt) == 0) atomicAdd(&deg[v], (uint32_t)__popc(peers));
+    const unsigned pu = __match_any_sync(kFull, u);  // keys sorted by u: long runs in a warp
+    if (valid && (pu & lt) == 0) atomicAdd(&deg[u], (uint32_t)__popc(pu));
+    const unsigned pv = __match_any_sync(kFull, v);
+    if (valid && (pv & lt) == 0) atomicAdd(&deg[v], (uint32_t)__popc(pv));
   }
+  heads = warp_sum(heads);
+  if (lane == 0 && heads) atomicAdd(m_out, (unsigned long long)heads);
 }
 
 struct ActivePred {
@@ -192,21 +191,26 @@ __global__ void k_prim_simple(const uint32_t* __restrict__ deg, uint64_t n, uint
   }
 }
 
-__global__ void k_shingle(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint32_t* __restrict__ sh) {
+__global__ void k_shingle(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
+                          uint32_t* __restrict__ sh) {
   const uint64_t mask = (1ull << b) - 1ull;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = (uint32_t)(keys[i] >> b), v = (uint32_t)(keys[i] & mask);
+    uint64_t k;
+    if (!key_head(keys, i, sentinel, k)) continue;
+    const uint32_t u = (uint32_t)(k >> b), v = (uint32_t)(k & mask);
     atomicMin(&sh[u], hash32(v));
     atomicMin(&sh[v], hash32(u));
   }
 }
 
 // undirected adjacency by id for the BFS orderings
-__global__ void k_adj_fill(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint64_t* __restrict__ off,
-                           uint32_t* __restrict__ cur, uint32_t* __restrict__ adj) {
+__global__ void k_adj_fill(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
+                           const uint64_t* __restrict__ off, uint32_t* __restrict__ cur, uint32_t* __restrict__ adj) {
   const uint64_t mask = (1ull << b) - 1ull;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = (uint32_t)(keys[i] >> b), v = (uint32_t)(keys[i] & mask);
+    uint64_t k;
+    if (!key_head(keys, i, sentinel, k)) continue;
+    const uint32_t u = (uint32_t)(k >> b), v = (uint32_t)(k & mask);
     adj[off[u] + atomicAdd(&cur[u], 1u)] = v;
     adj[off[v] + atomicAdd(&cur[v], 1u)] = u;
   }
@@ -246,8 +250,8 @@ __global__ void k_level_fix(uint32_t* __restrict__ level, uint64_t n, uint32_t u
 // a5: orient low rank -> high rank: out-degree histogram of the low end.
 // Keys arrive sorted by their low id, so runs of equal low ends are common
 // inside a warp: atomics are aggregated over equal targets (__match_any_sync).
-__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, const uint32_t* __restrict__ rank,
-                         uint32_t* __restrict__ dplus) {
+__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
+                         const uint32_t* __restrict__ rank, uint32_t* __restrict__ dplus) {
   const uint64_t mask = (1ull << b) - 1ull;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -255,10 +259,8 @@ __global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
     const uint64_t i = base + lane;
     uint32_t lo = 0xFFFFFFFFu;
-    if (i < m) {
-      const uint64_t k = keys[i];
-      lo = min(rank[k >> b], rank[k & mask]);
-    }
+    uint64_t k = 0;
+    if (i < m && key_head(keys, i, sentinel, k)) lo = min(rank[k >> b], rank[k & mask]);
     const unsigned peers = __match_any_sync(kFull, lo);
     if (lo != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&dplus[lo], (uint32_t)__popc(peers));
   }
@@ -267,7 +269,7 @@ __global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t
 // a5: counting-sort scatter of the high end into the low end's padded list
 // (slot order within a list is arbitrary; segmented_sort_u32 orders it).  One
 // cursor atomic per group of equal low ends in the warp.
-__global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b,
+__global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
                               const uint32_t* __restrict__ rank, const uint64_t* __restrict__ off16,
                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ col) {
   const uint64_t mask = (1ull << b) - 1ull;
@@ -277,8 +279,8 @@ __global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uin
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
     const uint64_t i = base + lane;
     uint32_t lo = 0xFFFFFFFFu, hi = 0;
-    if (i < m) {
-      const uint64_t k = keys[i];
+    uint64_t k = 0;
+    if (i < m && key_head(keys, i, sentinel, k)) {
       const uint32_t ru = rank[k >> b], rv = rank[k & mask];
       lo = min(ru, rv);
       hi = max(ru, rv);
@@ -318,15 +320,15 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* 
 
 // BFS levels from the highest-degree id over the undirected simple graph of the
 // distinct keys; ids not reached get the returned value (max level + 1).
-static uint32_t bfs_levels(const uint64_t* keys, uint64_t m, uint32_t b, const uint32_t* deg, uint64_t n_ids,
-                           uint32_t* level, Allocator& al, cudaStream_t s) {
+static uint32_t bfs_levels(const uint64_t* keys, uint64_t nk, uint64_t m, uint32_t b, uint64_t sentinel,
+                           const uint32_t* deg, uint64_t n_ids, uint32_t* level, Allocator& al, cudaStream_t s) {
   const unsigned TB = 256;
   DBuf<uint64_t> off(al, n_ids + 1), tot(al, 1);
   scan_exclusive_u32(deg, off.p, n_ids, tot.p, al, s);
   EH_CUDA(cudaMemcpyAsync(off.p + n_ids, tot.p, 8, cudaMemcpyDeviceToDevice, s));  // off[n] = 2m
   DBuf<uint32_t> cur(al, n_ids), adj(al, std::max<uint64_t>(1, 2 * m)), fa(al, n_ids), fb(al, n_ids), cnt(al, 1);
   EH_CUDA(cudaMemsetAsync(cur.p, 0, n_ids * 4, s));
-  k_adj_fill<<<grid_for(m, TB * 4), TB, 0, s>>>(keys, m, b, off.p, cur.p, adj.p);
+  k_adj_fill<<<grid_for(nk, TB * 4), TB, 0, s>>>(keys, nk, b, sentinel, off.p, cur.p, adj.p);
   EH_LAUNCH("k_adj_fill");
   DBuf<unsigned long long> best(al, 1);
   EH_CUDA(cudaMemsetAsync(best.p, 0, 8, s));
@@ -404,7 +406,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   // occupied slots (the downstream steps only need the DISTINCT edges); it was
   // measured slower on C3 (random DRAM sectors, and the unsorted output slows
   // the CSR scatter), so it is kept as an ablation.
-  uint64_t m = 0;
+  uint64_t m = 0, nk = 0;  // nk key entries; m of them are distinct non-loop edges
   DBuf<uint64_t> keys, alt;
   uint64_t* ukeys = nullptr;
   const char* dd_env = getenv("EH_DEDUP");
@@ -414,11 +416,9 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
     k_canon<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, keys.p);
     EH_LAUNCH("k_canon");
     mark("canon");
-    uint64_t* sk = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);
+    ukeys = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);  // consumed in place (key_head), no compaction
+    nk = n;
     mark("sort1");
-    uint64_t* other = (sk == keys.p) ? alt.p : keys.p;
-    m = select_if(n, UniqueKeyPred{sk, sentinel}, CopyKeyEmit{sk, other}, al, s);
-    ukeys = other;
   } else {
     uint32_t tbits = 10;
     while ((1ull << tbits) < n + n / 2 + n / 10) ++tbits;
@@ -429,26 +429,30 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
     mark("hash_insert");
     // m <= n: compact into an n-sized buffer
     keys = DBuf<uint64_t>(al, std::max<uint64_t>(1, n));
-    m = select_if(1ull << tbits, OccupiedPred{tab.p}, CopySlotEmit{tab.p, keys.p}, al, s);
+    nk = select_if(1ull << tbits, OccupiedPred{tab.p}, CopySlotEmit{tab.p, keys.p}, al, s);
     ukeys = keys.p;
   }
   msrc.reset();
   mdst.reset();
-  g->m = m;
   mark("dedup");
 
   // ---- a4: degree + (degree, id) rank
   DBuf<uint32_t> deg(al, n_ids);
   EH_CUDA(cudaMemsetAsync(deg.p, 0, n_ids * 4, s));
-  if (m) {
-    k_degree<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, deg.p);
+  DBuf<unsigned long long> dm(al, 2);  // {m, max degree}
+  EH_CUDA(cudaMemsetAsync(dm.p, 0, 16, s));
+  if (nk) {
+    k_degree<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, deg.p, dm.p);
     EH_LAUNCH("k_degree");
   }
-  DBuf<uint32_t> dmaxdeg(al, 1);
-  EH_CUDA(cudaMemsetAsync(dmaxdeg.p, 0, 4, s));
-  k_max_u32<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, dmaxdeg.p);
+  k_max_u32<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, reinterpret_cast<uint32_t*>(dm.p + 1));
   EH_LAUNCH("k_max_u32");
-  const uint32_t max_deg = read_scalar(dmaxdeg.p, s);
+  unsigned long long hm[2];
+  EH_CUDA(cudaMemcpyAsync(hm, dm.p, 16, cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  m = hm[0];
+  g->m = m;
+  const uint32_t max_deg = (uint32_t)hm[1];
   // NEXT-4: the primary rank key of the chosen node ordering (default: degree)
   DBuf<uint64_t> prim;
   uint32_t pbits = bitlen(max_deg);
@@ -459,12 +463,12 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
     if (g->order == EH_ORDER_SHINGLE) {
       aux = DBuf<uint32_t>(al, n_ids);
       EH_CUDA(cudaMemsetAsync(aux.p, 0xFF, n_ids * 4, s));
-      k_shingle<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, aux.p);
+      k_shingle<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, aux.p);
       EH_LAUNCH("k_shingle");
       pbits = 32;
     } else if (g->order == EH_ORDER_BFS || g->order == EH_ORDER_HYBRID) {
       aux = DBuf<uint32_t>(al, n_ids);
-      aux_max = bfs_levels(ukeys, m, b, deg.p, n_ids, aux.p, al, s);  // aux_max = level of unreached ids
+      aux_max = bfs_levels(ukeys, nk, m, b, sentinel, deg.p, n_ids, aux.p, al, s);  // level of unreached ids
       aux_bits = bitlen(aux_max);
       pbits = (g->order == EH_ORDER_BFS) ? aux_bits : bitlen(max_deg) + aux_bits;
     } else if (g->order == EH_ORDER_RANDOM) {
@@ -498,7 +502,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   DBuf<uint32_t> dplus(al, std::max<uint64_t>(1, n_act));
   EH_CUDA(cudaMemsetAsync(dplus.p, 0, std::max<uint64_t>(1, n_act) * 4, s));
   if (m) {
-    k_orient<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, dplus.p);
+    k_orient<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, rank.p, dplus.p);
     EH_LAUNCH("k_orient");
   }
   DBuf<uint64_t> off16(al, n_act + 1), tot(al, 1);
@@ -514,7 +518,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   mark("orient");
   if (m) {
     EH_CUDA(cudaMemsetAsync(p4.p, 0, std::max<uint64_t>(1, n_act) * 4, s));  // reuse as cursors
-    k_scatter_col<<<grid_for(m, TB * 4), TB, 0, s>>>(ukeys, m, b, rank.p, off16.p, p4.p, g->col);
+    k_scatter_col<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, rank.p, off16.p, p4.p, g->col);
     EH_LAUNCH("k_scatter_col");
   }
   deg.reset();
