@@ -36,9 +36,8 @@ constexpr int kWMaxD = 128;           // warp kernel: d <= 128 -> rows of <= 4 w
 constexpr int kWW = 4;                // row stride (words) in the warp kernel
 constexpr int kWHash = 512;           // hash slots >= 4d
 constexpr int kWWarps = 8;
-constexpr int kCMaxD = 1024;          // CTA kernel: d <= 1024 -> rows of <= 32 words
-constexpr int kCHash = 4096;
-constexpr int kCWarps = 16;
+constexpr int kCMaxD = 1024;          // CTA kernels: d <= 1024 -> rows of <= 32 words; two shapes
+                                      // (d <= 512: 8 warps, ~57 KB; larger: 16 warps, ~190 KB)
 constexpr uint32_t kEmptyK = 0xFFFFFFFFu;
 
 enum K4Kind : uint8_t { kKSkip = 0, kKProbe = 1, kKStream = 2, kKSearch = 3 };
@@ -204,32 +203,40 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
 }
 
 // ------------------------------------------------------------- CTA kernel --
-template <bool kU>
+template <int kMaxD, int kCWarps>
+constexpr size_t k4_cta_smem() {
+  return (size_t)(kMaxD + 4 * kMaxD + 2 * kMaxD + kMaxD * (kMaxD / 32 + 1)) * 4 + (size_t)kCWarps * kMaxD * 2;
+}
+
+// One CTA per x with dlo < d <= dhi (<= kMaxD); ctr slot `cslot` is its work cursor.
+template <bool kU, int kMaxD, int kCWarps>
 __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
-                                                          unsigned long long* __restrict__ ctr) {
+                                                          unsigned long long* __restrict__ ctr, uint32_t dlo,
+                                                          uint32_t cslot) {
+  constexpr int kCHash = 4 * kMaxD;
   extern __shared__ __align__(16) uint32_t dsm_k4c[];
-  uint32_t* xs = dsm_k4c;                                   // kCMaxD
-  uint32_t* hkeys = xs + kCMaxD;                            // kCHash
+  uint32_t* xs = dsm_k4c;                                   // kMaxD
+  uint32_t* hkeys = xs + kMaxD;                             // kCHash
   uint16_t* hidx = reinterpret_cast<uint16_t*>(hkeys + kCHash);  // kCHash u16
   uint32_t* L = hkeys + kCHash + kCHash / 2;                // d rows of S = W|1 words
-  uint16_t* jl_all = reinterpret_cast<uint16_t*>(L + kCMaxD * (kCMaxD / 32 + 1));  // per-warp edge lists
+  uint16_t* jl_all = reinterpret_cast<uint16_t*>(L + kMaxD * (kMaxD / 32 + 1));  // per-warp edge lists
   __shared__ unsigned long long s_wi;
   constexpr uint32_t kGroups = kCWarps * 32 / kG;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t gid = threadIdx.x / kG, gl = threadIdx.x % kG;
   unsigned long long cnt = 0;
   for (;;) {
-    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
+    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[cslot], 1ull);
     __syncthreads();
     const unsigned long long wi = s_wi;
     if (wi >= nwork) break;
     const uint32_t x = __ldg(work + wi);
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;
-    if (d > (uint32_t)kCMaxD || d < 3) {  // other classes handle these
+    if (d > (uint32_t)kMaxD || d <= dlo || d < 3) {  // the other shape / fallback handles these
       __syncthreads();
       continue;
     }
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
     // bit-parallel innermost loop: one warp per row i; the set bits j of L_i (the
     // local edges) are listed, then each LANE takes one edge and ANDs the words
     // of L_i and L_j above j (broadcast read of L_i, conflict-free reads of L_j).
-    uint16_t* jl = jl_all + w * kCMaxD;
+    uint16_t* jl = jl_all + w * kMaxD;
     for (uint32_t r = w; r < d; r += kCWarps) {
       const uint32_t* Li = L + r * S;
       const uint32_t wv = ((uint32_t)lane < W) ? Li[lane] : 0u;
@@ -291,8 +298,6 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
-constexpr size_t kCtaSmemK4 =
-    (size_t)(kCMaxD + kCHash + kCHash / 2 + kCMaxD * (kCMaxD / 32 + 1)) * 4 + (size_t)kCWarps * kCMaxD * 2;
 
 // ------------------------------------------- fallback: |N+(x)| > kCMaxD --
 // Rows (x, y = x_i) of the big x are flattened into one index space (prefix
@@ -367,15 +372,30 @@ __global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, 
 template <bool kU>
 uint64_t k4_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
-  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
+  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 8 * sizeof(unsigned long long), s));
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
   const uint64_t nlarge = g->n_work[2];
   const uint32_t* wl = g->work + nsmall;
   if (nlarge) {
-    EH_CUDA(cudaFuncSetAttribute(k_k4_cta<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemK4));
-    const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-    k_k4_cta<kU><<<grid, kCWarps * 32, kCtaSmemK4, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter);
-    EH_LAUNCH("k_k4_cta");
+    // d <= 512: 8-warp CTAs with ~57 KB (several per SM); 512 < d <= 1024: 16 warps, ~190 KB
+    {
+      constexpr size_t sm1 = k4_cta_smem<512, 8>();
+      auto k1 = k_k4_cta<kU, 512, 8>;
+      EH_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+      int per_sm = 0;
+      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 8 * 32, sm1));
+      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 2u);
+      EH_LAUNCH("k_k4_cta");
+    }
+    if (g->max_dplus > 512) {
+      constexpr size_t sm2 = k4_cta_smem<kCMaxD, 16>();
+      auto k2 = k_k4_cta<kU, kCMaxD, 16>;
+      EH_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
+      k2<<<grid, 16 * 32, sm2, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u);
+      EH_LAUNCH("k_k4_cta");
+    }
     if (g->max_dplus > (uint64_t)kCMaxD) {
       DBuf<uint32_t> bx(g->alloc, nlarge), brows(g->alloc, nlarge);
       const uint64_t nbig = select_if(nlarge, BigPred{g->desc, wl}, BigEmit{g->desc, wl, bx.p, brows.p}, g->alloc, s);
