@@ -36,8 +36,8 @@ constexpr int kWMaxD = 128;           // warp kernel: d <= 128 -> rows of <= 4 w
 constexpr int kWW = 4;                // row stride (words) in the warp kernel
 constexpr int kWHash = 512;           // hash slots >= 4d
 constexpr int kWWarps = 8;
-constexpr int kCMaxD = 1024;          // CTA kernels: d <= 1024 -> rows of <= 32 words; two shapes
-                                      // (d <= 512: 8 warps, ~57 KB; larger: 16 warps, ~190 KB)
+constexpr int kCMaxD = 1024;          // CTA kernels: d <= 1024 -> rows of <= 32 words; three shapes
+                                      // (d <= 256: 4 warps; <= 512: 8 warps, ~57 KB; larger: 16 warps, 192 KB)
 constexpr uint32_t kEmptyK = 0xFFFFFFFFu;
 
 enum K4Kind : uint8_t { kKSkip = 0, kKProbe = 1, kKStream = 2, kKSearch = 3 };
@@ -377,7 +377,17 @@ uint64_t k4_impl(eh_graph* g) {
   const uint64_t nlarge = g->n_work[2];
   const uint32_t* wl = g->work + nsmall;
   if (nlarge) {
-    // d <= 512: 8-warp CTAs with ~57 KB (several per SM); 512 < d <= 1024: 16 warps, ~190 KB
+    // d <= 256: 4-warp CTAs (~20 KB); d <= 512: 8-warp CTAs (~57 KB); 512 < d <= 1024: 16 warps, ~190 KB
+    {
+      constexpr size_t sm0 = k4_cta_smem<256, 4>();
+      auto k0 = k_k4_cta<kU, 256, 4>;
+      EH_CUDA(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
+      int per_sm = 0;
+      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k0, 4 * 32, sm0));
+      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+      k0<<<grid, 4 * 32, sm0, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 5u);
+      EH_LAUNCH("k_k4_cta");
+    }
     {
       constexpr size_t sm1 = k4_cta_smem<512, 8>();
       auto k1 = k_k4_cta<kU, 512, 8>;
@@ -385,7 +395,7 @@ uint64_t k4_impl(eh_graph* g) {
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 8 * 32, sm1));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 2u);
+      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u);
       EH_LAUNCH("k_k4_cta");
     }
     if (g->max_dplus > 512) {
