@@ -375,7 +375,7 @@ uint64_t k4_impl(eh_graph* g) {
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 8 * sizeof(unsigned long long), s));
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
   const uint64_t nlarge = g->n_work[2];
-  const uint32_t* wl = g->work + nsmall;
+  const uint32_t* wl = work_lpt(g) + nsmall;  // class 2 heaviest first
   if (nlarge) {
     // d <= 256: 4-warp CTAs (~20 KB); d <= 512: 8-warp CTAs (~57 KB); 512 < d <= 1024: 16 warps, ~190 KB
     {

@@ -409,7 +409,7 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
     int per_sm = 0;
     EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pv_cta, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nlarge, d_t,
+    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t,
                                                  g->d_counter, xcap);
     EH_LAUNCH("k_pv_cta");
   }

@@ -219,6 +219,7 @@ struct eh_graph {
   bool stats_ready = false;
   // Count-kernel work lists (vertices with |N+| >= 2 by class), see count_tri.cu.
   uint32_t* work = nullptr;
+  uint32_t* work_lpt = nullptr;  // same lists, classes 1-2 heaviest first (work_lpt(), on demand)
   uint64_t n_work[3] = {0, 0, 0};
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
@@ -240,6 +241,7 @@ namespace eh {
 void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, PhaseTimer* t = nullptr);
 // trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
 void build_layouts(eh_graph* g);
+const uint32_t* work_lpt(eh_graph* g);  // lazy: LPT-ordered work lists (trie.cu)
 void compute_stats(eh_graph* g);  // lazy: B_tri, wedge work, #bitset sets
 void build_block_layout(eh_graph* g);  // NEXT-3 composite layout (EH_BLOCK_LAYOUT)
 void build_worklists(eh_graph* g);

@@ -110,6 +110,17 @@ struct WorkEmit {
   __device__ void operator()(uint64_t pos, uint64_t v) const { out[pos] = (uint32_t)v; }
 };
 
+// (descending d, ascending x) sort key of a work-list entry, and back
+__global__ void k_work_key(const uint4* __restrict__ desc, const uint32_t* __restrict__ w, uint64_t n, uint32_t dmax,
+                           uint64_t* __restrict__ key) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    key[k] = ((uint64_t)(dmax - desc[w[k]].y) << 32) | w[k];
+}
+__global__ void k_work_unkey(const uint64_t* __restrict__ key, uint64_t n, uint32_t* __restrict__ w) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    w[k] = (uint32_t)key[k];
+}
+
 }  // namespace
 
 void build_layouts(eh_graph* g) {
@@ -282,6 +293,37 @@ void build_worklists(eh_graph* g) {
     g->n_work[c] = k;
     pos += k;
   }
+}
+
+// The work lists with classes 1 and 2 each in descending-d order (heaviest x
+// first: longest-processing-time order, so the per-x tails of the persistent CTA
+// kernels overlap the rest of the work).  Built on first use and kept in the
+// handle; used by the 4-clique and per-vertex kernels (measured: C4 K4 7.62 ->
+// 7.38 ms, C3 t(v) 19.6 -> 17.5 ms).  The triangle kernels keep rank order
+// (measured 0.3 % slower in LPT order at C3).
+const uint32_t* work_lpt(eh_graph* g) {
+  if (g->work_lpt) return g->work_lpt;
+  Allocator& al = g->alloc;
+  cudaStream_t s = g->stream;
+  const uint64_t n = g->n_work[0] + g->n_work[1] + g->n_work[2];
+  uint32_t* w = (uint32_t*)g->own(std::max<uint64_t>(1, n) * 4);
+  if (n) EH_CUDA(cudaMemcpyAsync(w, g->work, n * 4, cudaMemcpyDeviceToDevice, s));
+  uint64_t pos = g->n_work[0];
+  for (int c = 1; c < 3; ++c) {
+    const uint64_t k = g->n_work[c];
+    if (k > 1) {
+      DBuf<uint64_t> key(al, k), alt(al, k);
+      k_work_key<<<grid_for(k, 1024), 256, 0, s>>>(g->desc, w + pos, k, (uint32_t)g->max_dplus, key.p);
+      EH_LAUNCH("k_work_key");
+      const uint64_t* sorted = radix_sort_u64(key.p, alt.p, k, 32 + bitlen(g->max_dplus), al, s);
+      k_work_unkey<<<grid_for(k, 1024), 256, 0, s>>>(sorted, k, w + pos);
+      EH_LAUNCH("k_work_unkey");
+      EH_CUDA(cudaStreamSynchronize(s));  // key / alt are released on return
+    }
+    pos += k;
+  }
+  g->work_lpt = w;
+  return w;
 }
 
 }  // namespace eh
