@@ -126,7 +126,11 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 // LSD radix sort of u64 keys over bits [0, key_bits), 8-bit digits, stable.
 // Returns the buffer holding the result (keys or alt).
 uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
-                         cudaStream_t s);
+                         cudaStream_t s, uint32_t begin_bit = 0);
+// a1 + a2 fused: sort the canonical keys (min << b) | max of (src[i], dst[i]) (self-loops -> the
+// all-ones sentinel of 2b bits) without materialising them first; keys / alt: n-element buffers
+uint64_t* radix_sort_canon(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t b, uint64_t* keys,
+                           uint64_t* alt, Allocator& al, cudaStream_t s);
 // Sort segment v = data[off16[v]*4 .. + len[v]) in place for v < nseg (segsort.cu).
 void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
                         Allocator& al, cudaStream_t s);

@@ -46,16 +46,6 @@ __global__ void k_dict_map(const uint32_t* __restrict__ in, uint32_t* __restrict
   }
 }
 
-// a1: canonical undirected key (min << b) | max; self-loops -> all-ones sentinel.
-__global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
-                        uint32_t b, uint64_t* __restrict__ keys) {
-  const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = src[i], v = dst[i];
-    keys[i] = (u == v) ? sentinel : (((uint64_t)min(u, v) << b) | (uint64_t)max(u, v));
-  }
-}
-
 // a1-a3 fused: canonical key (min << b) | max of every non-loop pair inserted
 // into an open-addressing hash set (linear probing; read before CAS, so the
 // duplicates that are already present cost no atomic).  Empty slot = all ones,
@@ -413,10 +403,9 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   if (!(dd_env && strcmp(dd_env, "hash") == 0)) {
     keys = DBuf<uint64_t>(al, n);
     alt = DBuf<uint64_t>(al, n);
-    k_canon<<<grid_for(n, TB * 4), TB, 0, s>>>(usrc, udst, n, b, keys.p);
-    EH_LAUNCH("k_canon");
-    mark("canon");
-    ukeys = radix_sort_u64(keys.p, alt.p, n, 2 * b, al, s);  // consumed in place (key_head), no compaction
+    // a1 canonicalisation fused into the sort's histogram and first pass; the
+    // sorted keys are consumed in place (key_head), no compaction
+    ukeys = radix_sort_canon(usrc, udst, n, b, keys.p, alt.p, al, s);
     nk = n;
     mark("sort1");
   } else {
@@ -483,7 +472,9 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
       ralt(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m)));
   const uint64_t n_act = select_if(n_ids, ActivePred{deg.p}, RankKeyEmit{prim.p, deg.p, b, rkeys.p}, al, s);
   g->n_act = n_act;
-  uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + pbits, al, s);
+  // select_if emits the ids in ascending order and LSD radix passes are stable:
+  // sorting by the primary bits alone gives the (primary, id) order
+  uint64_t* rsorted = radix_sort_u64(rkeys.p, ralt.p, n_act, b + pbits, al, s, b);
   prim.reset();
   DBuf<uint32_t>& rank = deg;  // k_rank turns deg[id] into rank[id] (and records deg per rank)
   g->orig_id = (uint32_t*)g->own(std::max<uint64_t>(1, n_act) * 4);

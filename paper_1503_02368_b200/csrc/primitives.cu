@@ -101,15 +101,40 @@ constexpr int kRDigits = 256;
 constexpr int kRMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-// (1) all-pass digit histograms in one read
+// Key source of the first pass: the keys themselves, or (kCanon, SURVEY.md §8(a)
+// row a1 fused into the sort) the canonical undirected key (min << b) | max of
+// the pair (src[i], dst[i]), self-loops mapped to the all-ones sentinel.
+struct CanonSrc {
+  const uint32_t* src;
+  const uint32_t* dst;
+  uint32_t b;
+  uint64_t sentinel;
+};
+template <typename K, bool kCanon>
+__device__ __forceinline__ K load_key(const K* __restrict__ keys, const CanonSrc& cs, uint64_t i) {
+  if (kCanon) {
+    const uint32_t u = __ldg(cs.src + i), v = __ldg(cs.dst + i);
+    return (u == v) ? (K)cs.sentinel : (K)((((uint64_t)min(u, v)) << cs.b) | (uint64_t)max(u, v));
+  }
+  return keys[i];
+}
+
 template <typename K>
-__global__ void __launch_bounds__(kRBlock) k_radix_hist(const K* __restrict__ keys, uint64_t n, uint32_t passes,
+__global__ void k_canon_fill(CanonSrc cs, uint64_t n, K* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = load_key<K, true>(out, cs, i);
+}
+
+// (1) all-pass digit histograms in one read (digits start at bit `begin`)
+template <typename K, bool kCanon>
+__global__ void __launch_bounds__(kRBlock) k_radix_hist(const K* __restrict__ keys, CanonSrc cs, uint64_t n,
+                                                        uint32_t passes, uint32_t begin,
                                                         unsigned long long* __restrict__ hist) {
   __shared__ uint32_t h[kRMaxPasses][kRDigits];
   for (int i = threadIdx.x; i < kRMaxPasses * kRDigits; i += kRBlock) (&h[0][0])[i] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * kRBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kRBlock) {
-    const K k = keys[i];
+    const K k = load_key<K, kCanon>(keys, cs, i) >> begin;
     for (uint32_t p = 0; p < passes; ++p) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 0xFFu], 1u);
   }
   __syncthreads();
@@ -133,8 +158,9 @@ __global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long lon
 }
 
 // (2) one pass
-template <typename K, int kPBlock, int kRItems>
-__global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, K* __restrict__ out, uint64_t n,
+template <typename K, int kPBlock, int kRItems, bool kCanon>
+__global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
+                                                                           K* __restrict__ out, uint64_t n,
                                                         uint32_t shift, const unsigned long long* __restrict__ base,
                                                         unsigned long long* __restrict__ status,
                                                         uint32_t* __restrict__ tile_ctr) {
@@ -160,7 +186,7 @@ __global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const
   for (int r = 0; r < kRItems; ++r) {
     const uint32_t li = (uint32_t)w * 32 * kRItems + (uint32_t)r * 32 + lane;
     const bool valid = li < tn;
-    key[r] = valid ? in[t0 + li] : K(0);
+    key[r] = valid ? load_key<K, kCanon>(in, cs, t0 + li) : K(0);
     const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 0xFFu) : 0x100u;
     const unsigned peers = __match_any_sync(kFull, d);
     const uint32_t before = (d < 0x100u) ? wcnt[w][d] : 0u;
@@ -239,16 +265,52 @@ __global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const
   }
 }
 
+template <typename K, int kPBlock, int kRItems, bool kCanon>
+static void launch_pass(const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift, const unsigned long long* bp,
+                        unsigned long long* status, uint32_t* ctr, uint64_t tiles, size_t smem, cudaStream_t s) {
+  auto k = k_radix_pass<K, kPBlock, kRItems, kCanon>;
+  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)tiles, kPBlock, smem, s>>>(src, cs, dst, n, shift, bp, status, ctr);
+  EH_LAUNCH("k_radix_pass");
+}
+
+template <typename K, bool kCanon>
+static void launch_pass_cfg(int cfg, const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift,
+                            const unsigned long long* bp, unsigned long long* status, uint32_t* ctr, uint64_t tiles,
+                            size_t smem, cudaStream_t s) {
+  switch (cfg) {
+    case 0: launch_pass<K, 512, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    case 1: launch_pass<K, 256, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    case 2: launch_pass<K, 256, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    default: launch_pass<K, 512, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+  }
+}
+
+// LSD sort of keys by bits [begin, key_bits).  Stable, so a key array already
+// ordered by its low `begin` bits comes out ordered by the whole key.  With
+// cs.src != nullptr (u64 only) the keys are produced from (src, dst) by the
+// histogram and the first non-trivial pass (the canonicalisation of row a1 fused
+// into the sort); `keys` is then only an output buffer.
 template <typename K>
-static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& al, cudaStream_t s) {
-  if (n <= 1 || key_bits == 0) return keys;
-  const uint32_t passes = (key_bits + 7) / 8;
+static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t begin, CanonSrc cs, Allocator& al,
+                     cudaStream_t s) {
+  const bool canon = cs.src != nullptr;
+  if (n == 0) return keys;
+  if (key_bits <= begin || n == 1) {
+    if (canon) {
+      k_canon_fill<K><<<grid_for(n, 1024), 256, 0, s>>>(cs, n, keys);
+      EH_LAUNCH("k_canon_fill");
+    }
+    return keys;
+  }
+  const uint32_t passes = (key_bits - begin + 7) / 8;
   DBuf<unsigned long long> hist(al, (size_t)passes * kRDigits), base(al, (size_t)passes * kRDigits);
   DBuf<uint32_t> trivial(al, kRMaxPasses), ctr(al, kRMaxPasses);
   EH_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes(), s));
   EH_CUDA(cudaMemsetAsync(trivial.p, 0, trivial.bytes(), s));
   EH_CUDA(cudaMemsetAsync(ctr.p, 0, ctr.bytes(), s));
-  k_radix_hist<K><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, n, passes, hist.p);
+  if (canon) k_radix_hist<K, true><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, hist.p);
+  else k_radix_hist<K, false><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, hist.p);
   EH_LAUNCH("k_radix_hist");
   k_radix_base<<<passes, kRDigits, 0, s>>>(hist.p, base.p, trivial.p, n);
   EH_LAUNCH("k_radix_base");
@@ -264,43 +326,38 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, Allocator& 
   if (tiles >= (1ull << 31)) fail(EH_EINVAL, "radix sort: too many keys");
   DBuf<unsigned long long> status(al, (size_t)tiles * kRDigits);
   const size_t smem = tile * sizeof(K);
+  // the canonical source is read by the first non-trivial pass, which writes `keys`
+  bool from_src = canon;
   K* src = keys;
-  K* dst = alt;
+  K* dst = canon ? keys : alt;
   for (uint32_t p = 0; p < passes; ++p) {
     if (triv[p]) continue;
     EH_CUDA(cudaMemsetAsync(status.p, 0, status.bytes(), s));
     const unsigned long long* bp = base.p + (size_t)p * kRDigits;
-    switch (cfg) {
-      case 0:
-        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_radix_pass<K, 512, 8><<<(unsigned)tiles, 512, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
-        break;
-      case 1:
-        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_radix_pass<K, 256, 8><<<(unsigned)tiles, 256, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
-        break;
-      case 2:
-        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_radix_pass<K, 256, 16><<<(unsigned)tiles, 256, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
-        break;
-      default:
-        EH_CUDA(cudaFuncSetAttribute(k_radix_pass<K, 512, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_radix_pass<K, 512, 16><<<(unsigned)tiles, 512, smem, s>>>(src, dst, n, 8 * p, bp, status.p, ctr.p + p);
-        break;
-    }
-    EH_LAUNCH("k_radix_pass");
+    if (from_src) launch_pass_cfg<K, true>(cfg, nullptr, cs, dst, n, begin + 8 * p, bp, status.p, ctr.p + p, tiles, smem, s);
+    else launch_pass_cfg<K, false>(cfg, src, cs, dst, n, begin + 8 * p, bp, status.p, ctr.p + p, tiles, smem, s);
+    if (from_src) { from_src = false; src = keys; dst = alt; continue; }
     K* t = src; src = dst; dst = t;
+  }
+  if (from_src) {  // every pass trivial: materialise the keys (already in order)
+    k_canon_fill<K><<<grid_for(n, 1024), 256, 0, s>>>(cs, n, keys);
+    EH_LAUNCH("k_canon_fill");
   }
   return src;
 }
 
 uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
-                         cudaStream_t s) {
-  return radix_impl<uint64_t>(keys, alt, n, key_bits, al, s);
+                         cudaStream_t s, uint32_t begin_bit) {
+  return radix_impl<uint64_t>(keys, alt, n, key_bits, begin_bit, CanonSrc{nullptr, nullptr, 0, 0}, al, s);
 }
 uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s) {
-  return radix_impl<uint32_t>(keys, alt, n, key_bits, al, s);
+  return radix_impl<uint32_t>(keys, alt, n, key_bits, 0, CanonSrc{nullptr, nullptr, 0, 0}, al, s);
+}
+uint64_t* radix_sort_canon(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t b, uint64_t* keys,
+                           uint64_t* alt, Allocator& al, cudaStream_t s) {
+  const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
+  return radix_impl<uint64_t>(keys, alt, n, 2 * b, 0, CanonSrc{src, dst, b, sentinel}, al, s);
 }
 
 }  // namespace eh
