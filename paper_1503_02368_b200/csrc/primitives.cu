@@ -4,7 +4,7 @@
 // the (degree, id) rank sort, dictionary encoding) and by the layout / work-list
 // builders.
 //
-// Radix sort = one-sweep LSD with 8-bit digits:
+// Radix sort = one-sweep LSD with 8-bit digits (9-bit when that saves a pass):
 //   (1) one read of the keys builds the digit histograms of EVERY pass;
 //       an exclusive scan per pass gives each digit's global base;
 //   (2) per pass, tiles of 4096 keys are taken in launch order from an atomic
@@ -97,7 +97,7 @@ void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t*
 // ------------------------------------------------------------- radix sort --
 constexpr int kRBlock = 256;                  // histogram kernel
 constexpr int kRadixDefaultCfg = 2;           // pass kernel tile: 256 threads x 16 keys (measured best, see radix_impl)
-constexpr int kRDigits = 256;
+constexpr int kRMaxDigits = 512;              // digits of 8 or 9 bits
 constexpr int kRMaxPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
@@ -125,172 +125,200 @@ __global__ void k_canon_fill(CanonSrc cs, uint64_t n, K* __restrict__ out) {
     out[i] = load_key<K, true>(out, cs, i);
 }
 
-// (1) all-pass digit histograms in one read (digits start at bit `begin`)
+// (1) all-pass digit histograms in one read (pass p: bits [begin + p*bits, +bits))
 template <typename K, bool kCanon>
 __global__ void __launch_bounds__(kRBlock) k_radix_hist(const K* __restrict__ keys, CanonSrc cs, uint64_t n,
-                                                        uint32_t passes, uint32_t begin,
+                                                        uint32_t passes, uint32_t begin, uint32_t bits,
                                                         unsigned long long* __restrict__ hist) {
-  __shared__ uint32_t h[kRMaxPasses][kRDigits];
-  for (int i = threadIdx.x; i < kRMaxPasses * kRDigits; i += kRBlock) (&h[0][0])[i] = 0;
+  __shared__ uint32_t h[kRMaxPasses * kRMaxDigits];
+  const uint32_t nd = 1u << bits, dm = nd - 1u;
+  for (int i = threadIdx.x; i < kRMaxPasses * kRMaxDigits; i += kRBlock) h[i] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * kRBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kRBlock) {
     const K k = load_key<K, kCanon>(keys, cs, i) >> begin;
-    for (uint32_t p = 0; p < passes; ++p) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 0xFFu], 1u);
+    for (uint32_t p = 0; p < passes; ++p) atomicAdd(&h[p * nd + ((uint32_t)(k >> (bits * p)) & dm)], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)passes * kRDigits; i += kRBlock) {
-    const uint32_t c = (&h[0][0])[i];
+  for (int i = threadIdx.x; i < (int)(passes * nd); i += kRBlock) {
+    const uint32_t c = h[i];
     if (c) atomicAdd(&hist[i], (unsigned long long)c);
   }
 }
 
-// per-pass exclusive scan of the 256 digit counts (one CTA of 256 threads per pass)
-__global__ void __launch_bounds__(kRDigits) k_radix_base(const unsigned long long* __restrict__ hist,
-                                                         unsigned long long* __restrict__ base,
-                                                         uint32_t* __restrict__ trivial, uint64_t n) {
-  __shared__ unsigned long long sw[kRDigits / 32 + 1];
+// per-pass exclusive scan of the digit counts (one CTA per pass, one thread per digit)
+__global__ void __launch_bounds__(kRMaxDigits) k_radix_base(const unsigned long long* __restrict__ hist,
+                                                            unsigned long long* __restrict__ base,
+                                                            uint32_t* __restrict__ trivial, uint64_t n, uint32_t nd) {
+  __shared__ unsigned long long sw[kRMaxDigits / 32 + 1];
   const uint32_t p = blockIdx.x;
-  const unsigned long long c = hist[p * kRDigits + threadIdx.x];
+  const unsigned long long c = (threadIdx.x < nd) ? hist[p * nd + threadIdx.x] : 0ull;
   unsigned long long tot;
-  const unsigned long long ex = block_exclusive_scan<kRDigits>(c, sw, &tot);
-  base[p * kRDigits + threadIdx.x] = ex;
+  const unsigned long long ex = block_exclusive_scan<kRMaxDigits>(c, sw, &tot);
+  if (threadIdx.x < nd) base[p * nd + threadIdx.x] = ex;
   if (c == n) trivial[p] = 1u;  // every key has this digit: the pass is the identity
 }
 
-// (2) one pass
-template <typename K, int kPBlock, int kRItems, bool kCanon>
+// (2) one pass over digits of kBits bits
+template <typename K, int kBits, int kPBlock, int kRItems, bool kCanon>
 __global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
                                                                            K* __restrict__ out, uint64_t n,
-                                                        uint32_t shift, const unsigned long long* __restrict__ base,
-                                                        unsigned long long* __restrict__ status,
-                                                        uint32_t* __restrict__ tile_ctr) {
+                                                                           uint32_t shift,
+                                                                           const unsigned long long* __restrict__ base,
+                                                                           unsigned long long* __restrict__ status,
+                                                                           uint32_t* __restrict__ tile_ctr) {
+  constexpr int kD = 1 << kBits;
+  constexpr uint32_t kDM = kD - 1, kInv = kD;    // digit mask, invalid-key marker
+  constexpr int kDPT = kD > kPBlock ? kD / kPBlock : 1;  // consecutive digits per thread
+  static_assert(kD <= kPBlock * kDPT, "digits per thread");
   constexpr int kRWarps = kPBlock / 32;
   constexpr int kRTile = kPBlock * kRItems;
   extern __shared__ __align__(16) unsigned char dsm_radix[];
   K* skeys = reinterpret_cast<K*>(dsm_radix);    // kRTile keys (dynamic shared memory)
-  __shared__ uint16_t wcnt[kRWarps][kRDigits];   // per-warp digit counts (<= 32 * items), then prefixes
-  __shared__ uint32_t tdp[kRDigits];             // tile-local exclusive digit prefix
-  __shared__ unsigned long long goff[kRDigits];  // global position of the tile's first key with digit d
+  __shared__ uint16_t wcnt[kRWarps][kD];         // per-warp digit counts (<= 32 * items), then prefixes
+  __shared__ uint32_t tdp[kD];                   // tile-local exclusive digit prefix
+  __shared__ unsigned long long goff[kD];        // global position of the tile's first key with digit d
   __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < kRWarps * kRDigits; i += kPBlock) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kRWarps * kD; i += kPBlock) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t t0 = tile * kRTile;
   const uint64_t tn = min((uint64_t)kRTile, n - t0);
   const unsigned lt = (1u << lane) - 1u;
   K key[kRItems];
-  uint32_t rd[kRItems];  // rank within the warp sub-tile (low 16 bits) | digit << 16 (0x100: invalid)
+  uint32_t rd[kRItems];  // rank within the warp sub-tile (low 16 bits) | digit << 16 (kInv: invalid)
 #pragma unroll
   for (int r = 0; r < kRItems; ++r) {
     const uint32_t li = (uint32_t)w * 32 * kRItems + (uint32_t)r * 32 + lane;
     const bool valid = li < tn;
     key[r] = valid ? load_key<K, kCanon>(in, cs, t0 + li) : K(0);
-    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & 0xFFu) : 0x100u;
+    const uint32_t d = valid ? ((uint32_t)(key[r] >> shift) & kDM) : kInv;
     const unsigned peers = __match_any_sync(kFull, d);
-    const uint32_t before = (d < 0x100u) ? wcnt[w][d] : 0u;
+    const uint32_t before = (d < kInv) ? wcnt[w][d] : 0u;
     __syncwarp();
-    if (d < 0x100u && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(before + __popc(peers));
+    if (d < kInv && (peers & lt) == 0) wcnt[w][d] = (uint16_t)(before + __popc(peers));
     __syncwarp();
     rd[r] = (before + __popc(peers & lt)) | (d << 16);
   }
   __syncthreads();
-  // thread d < 256: per-warp exclusive prefix, tile total, look-back
-  const uint32_t d = threadIdx.x;
-  uint32_t total = 0;
-  if (d < kRDigits) {
-    uint32_t run = 0;
+  // thread t owns digits [t*kDPT, t*kDPT + kDPT): per-warp exclusive prefix, tile totals
+  const uint32_t d0 = threadIdx.x * kDPT;
+  const bool owner = d0 < (uint32_t)kD;
+  uint32_t total[kDPT];
+  uint32_t tsum = 0;
 #pragma unroll
-    for (int ww = 0; ww < kRWarps; ++ww) {
-      const uint32_t c = wcnt[ww][d];
-      wcnt[ww][d] = (uint16_t)run;  // prefix <= 4096 fits u16
-      run += c;
+  for (int q = 0; q < kDPT; ++q) {
+    total[q] = 0;
+    if (owner) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kRWarps; ++ww) {
+        const uint32_t c = wcnt[ww][d0 + q];
+        wcnt[ww][d0 + q] = (uint16_t)run;  // prefix <= tile size fits u16
+        run += c;
+      }
+      total[q] = run;
+      // publish this tile's aggregate (tile 0: its inclusive prefix)
+      __stcg(status + tile * kD + d0 + q, (tile == 0 ? kFlagInc : kFlagAgg) | run);
+      if (tile == 0) goff[d0 + q] = base[d0 + q];
     }
-    total = run;
+    tsum += total[q];
   }
-  // publish this tile's aggregate (tile 0: its inclusive prefix) for every digit
-  __shared__ uint32_t stot[kRDigits];
-  if (d < kRDigits) {
-    stot[d] = total;
-    __stcg(status + tile * kRDigits + d, (tile == 0 ? kFlagInc : kFlagAgg) | total);
-    if (tile == 0) goff[d] = base[d];
-  }
+  // the barrier also keeps the compiler from merging the aggregate store above
+  // with the inclusive store below (same address): without the early aggregate
+  // the look-back degenerates into a serial chain
   __syncthreads();
   // decoupled look-back, one thread per digit, reading a window of 8 preceding
   // tiles per step (independent loads in flight); a tile that has not published
   // yet stops the window and is re-read from there.
-  if (tile > 0 && d < kRDigits) {
-    constexpr int kW = 8;
-    unsigned long long excl = 0;
-    int64_t t = (int64_t)tile - 1;
-    for (;;) {
-      unsigned long long sv[kW];
+  if (tile > 0 && owner) {
 #pragma unroll
-      for (int j = 0; j < kW; ++j)
-        sv[j] = (t - j >= 0) ? *((volatile unsigned long long*)(status + (uint64_t)(t - j) * kRDigits + d)) : kFlagInc;
-      int j = 0;
-      bool done = false;
+    for (int q = 0; q < kDPT; ++q) {
+      const uint32_t d = d0 + q;
+      constexpr int kW = 8;
+      unsigned long long excl = 0;
+      int64_t t = (int64_t)tile - 1;
+      for (;;) {
+        unsigned long long sv[kW];
 #pragma unroll
-      for (int q = 0; q < kW; ++q) {
-        if (done || j != q) continue;
-        const unsigned long long fl = sv[q] & ~kValMask;
-        if (fl == 0) continue;  // not published yet: stop the window here
-        excl += sv[q] & kValMask;
-        ++j;
-        if (fl == kFlagInc) done = true;
+        for (int j = 0; j < kW; ++j)
+          sv[j] = (t - j >= 0) ? *((volatile unsigned long long*)(status + (uint64_t)(t - j) * kD + d)) : kFlagInc;
+        int j = 0;
+        bool done = false;
+#pragma unroll
+        for (int q2 = 0; q2 < kW; ++q2) {
+          if (done || j != q2) continue;
+          const unsigned long long fl = sv[q2] & ~kValMask;
+          if (fl == 0) continue;  // not published yet: stop the window here
+          excl += sv[q2] & kValMask;
+          ++j;
+          if (fl == kFlagInc) done = true;
+        }
+        if (done) break;
+        t -= j;
       }
-      if (done) break;
-      t -= j;
+      __stcg(status + tile * kD + d, kFlagInc | (excl + total[q]));
+      goff[d] = base[d] + excl;
     }
-    __stcg(status + tile * kRDigits + d, kFlagInc | (excl + total));
-    goff[d] = base[d] + excl;
   }
-  // tile-local exclusive prefix over digits (threads >= 256 contribute 0)
+  // tile-local exclusive prefix over digits (threads without digits contribute 0)
   {
     __shared__ uint32_t sw[kPBlock / 32 + 1];
     uint32_t tt;
-    const uint32_t ex = block_exclusive_scan<kPBlock>(total, sw, &tt);
-    if (d < kRDigits) tdp[d] = ex;
+    uint32_t ex = block_exclusive_scan<kPBlock>(tsum, sw, &tt);
+    if (owner) {
+#pragma unroll
+      for (int q = 0; q < kDPT; ++q) { tdp[d0 + q] = ex; ex += total[q]; }
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRItems; ++r)
-    if ((rd[r] >> 16) < 0x100u) skeys[tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu)] = key[r];
+    if ((rd[r] >> 16) < kInv) skeys[tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu)] = key[r];
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < tn; i += kPBlock) {
     const K k = skeys[i];
-    const uint32_t dd = (uint32_t)(k >> shift) & 0xFFu;
+    const uint32_t dd = (uint32_t)(k >> shift) & kDM;
     out[goff[dd] + (i - tdp[dd])] = k;
   }
 }
 
-template <typename K, int kPBlock, int kRItems, bool kCanon>
+template <typename K, int kBits, int kPBlock, int kRItems, bool kCanon>
 static void launch_pass(const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift, const unsigned long long* bp,
                         unsigned long long* status, uint32_t* ctr, uint64_t tiles, size_t smem, cudaStream_t s) {
-  auto k = k_radix_pass<K, kPBlock, kRItems, kCanon>;
+  auto k = k_radix_pass<K, kBits, kPBlock, kRItems, kCanon>;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)tiles, kPBlock, smem, s>>>(src, cs, dst, n, shift, bp, status, ctr);
   EH_LAUNCH("k_radix_pass");
 }
 
-template <typename K, bool kCanon>
+template <typename K, int kBits, bool kCanon>
 static void launch_pass_cfg(int cfg, const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift,
                             const unsigned long long* bp, unsigned long long* status, uint32_t* ctr, uint64_t tiles,
                             size_t smem, cudaStream_t s) {
   switch (cfg) {
-    case 0: launch_pass<K, 512, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
-    case 1: launch_pass<K, 256, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
-    case 2: launch_pass<K, 256, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
-    default: launch_pass<K, 512, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    case 0: launch_pass<K, kBits, 512, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    case 1: launch_pass<K, kBits, 256, 8, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    case 2: launch_pass<K, kBits, 256, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
+    default: launch_pass<K, kBits, 512, 16, kCanon>(src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s); break;
   }
+}
+
+template <typename K, bool kCanon>
+static void launch_pass_bits(uint32_t bits, int cfg, const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift,
+                             const unsigned long long* bp, unsigned long long* status, uint32_t* ctr, uint64_t tiles,
+                             size_t smem, cudaStream_t s) {
+  if (bits == 9) launch_pass_cfg<K, 9, kCanon>(cfg, src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s);
+  else launch_pass_cfg<K, 8, kCanon>(cfg, src, cs, dst, n, shift, bp, status, ctr, tiles, smem, s);
 }
 
 // LSD sort of keys by bits [begin, key_bits).  Stable, so a key array already
 // ordered by its low `begin` bits comes out ordered by the whole key.  With
 // cs.src != nullptr (u64 only) the keys are produced from (src, dst) by the
 // histogram and the first non-trivial pass (the canonicalisation of row a1 fused
-// into the sort); `keys` is then only an output buffer.
+// into the sort); `keys` is then only an output buffer.  Digits are 8 bits, or 9
+// when that saves a pass (EH_RADIX_BITS=8|9 forces one).
 template <typename K>
 static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t begin, CanonSrc cs, Allocator& al,
                      cudaStream_t s) {
@@ -303,28 +331,40 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t be
     }
     return keys;
   }
-  const uint32_t passes = (key_bits - begin + 7) / 8;
-  DBuf<unsigned long long> hist(al, (size_t)passes * kRDigits), base(al, (size_t)passes * kRDigits);
+  const uint32_t span = key_bits - begin;
+  // 9-bit digits when they save a pass, with the 8192-key tile (its longer digit
+  // runs pay for the 512 buckets); the 8192-key tile also for very large inputs.
+  // Measured (tools/radix_bench.cu, B200): C3 keys (44 bits) 8-bit/4096 4.07 ms,
+  // 9-bit/8192 3.95 ms; C5 keys (52 bits) 8-bit 110 / 92 ms (4096 / 8192), 9-bit/8192 88.7 ms.
+  uint32_t bits = ((span + 8) / 9 < (span + 7) / 8) ? 9u : 8u;
+  if (const char* e = getenv("EH_RADIX_BITS")) bits = (atoi(e) == 9) ? 9u : 8u;
+  const uint32_t nd = 1u << bits;
+  const uint32_t passes = (span + bits - 1) / bits;
+  if (passes > (uint32_t)kRMaxPasses) fail(EH_EINVAL, "radix sort: %u key bits", span);
+  DBuf<unsigned long long> hist(al, (size_t)passes * nd), base(al, (size_t)passes * nd);
   DBuf<uint32_t> trivial(al, kRMaxPasses), ctr(al, kRMaxPasses);
   EH_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes(), s));
   EH_CUDA(cudaMemsetAsync(trivial.p, 0, trivial.bytes(), s));
   EH_CUDA(cudaMemsetAsync(ctr.p, 0, ctr.bytes(), s));
-  if (canon) k_radix_hist<K, true><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, hist.p);
-  else k_radix_hist<K, false><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, hist.p);
+  if (canon)
+    k_radix_hist<K, true><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, bits, hist.p);
+  else
+    k_radix_hist<K, false><<<grid_for(n, kRBlock * 16, kSMs * 8), kRBlock, 0, s>>>(keys, cs, n, passes, begin, bits, hist.p);
   EH_LAUNCH("k_radix_hist");
-  k_radix_base<<<passes, kRDigits, 0, s>>>(hist.p, base.p, trivial.p, n);
+  k_radix_base<<<passes, kRMaxDigits, 0, s>>>(hist.p, base.p, trivial.p, n, nd);
   EH_LAUNCH("k_radix_base");
   uint32_t triv[kRMaxPasses];
   EH_CUDA(cudaMemcpyAsync(triv, trivial.p, sizeof triv, cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   // tile shape (threads x keys per thread); EH_RADIX_CFG selects one for tuning
   static const int cfg_env = [] { const char* e = getenv("EH_RADIX_CFG"); return e ? atoi(e) : -1; }();
-  const int cfg = (cfg_env >= 0 && cfg_env <= 3) ? cfg_env : kRadixDefaultCfg;
+  const int cfg = (cfg_env >= 0 && cfg_env <= 3) ? cfg_env
+                  : (bits == 9 || n >= (1ull << 28)) ? 3 : kRadixDefaultCfg;
   static const int kThreads[4] = {512, 256, 256, 512}, kItems[4] = {8, 8, 16, 16};
   const uint64_t tile = (uint64_t)kThreads[cfg] * kItems[cfg];
   const uint64_t tiles = (n + tile - 1) / tile;
   if (tiles >= (1ull << 31)) fail(EH_EINVAL, "radix sort: too many keys");
-  DBuf<unsigned long long> status(al, (size_t)tiles * kRDigits);
+  DBuf<unsigned long long> status(al, (size_t)tiles * nd);
   const size_t smem = tile * sizeof(K);
   // the canonical source is read by the first non-trivial pass, which writes `keys`
   bool from_src = canon;
@@ -333,9 +373,10 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t be
   for (uint32_t p = 0; p < passes; ++p) {
     if (triv[p]) continue;
     EH_CUDA(cudaMemsetAsync(status.p, 0, status.bytes(), s));
-    const unsigned long long* bp = base.p + (size_t)p * kRDigits;
-    if (from_src) launch_pass_cfg<K, true>(cfg, nullptr, cs, dst, n, begin + 8 * p, bp, status.p, ctr.p + p, tiles, smem, s);
-    else launch_pass_cfg<K, false>(cfg, src, cs, dst, n, begin + 8 * p, bp, status.p, ctr.p + p, tiles, smem, s);
+    const unsigned long long* bp = base.p + (size_t)p * nd;
+    const uint32_t shift = begin + bits * p;
+    if (from_src) launch_pass_bits<K, true>(bits, cfg, nullptr, cs, dst, n, shift, bp, status.p, ctr.p + p, tiles, smem, s);
+    else launch_pass_bits<K, false>(bits, cfg, src, cs, dst, n, shift, bp, status.p, ctr.p + p, tiles, smem, s);
     if (from_src) { from_src = false; src = keys; dst = alt; continue; }
     K* t = src; src = dst; dst = t;
   }
