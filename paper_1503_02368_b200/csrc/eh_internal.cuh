@@ -225,6 +225,7 @@ struct eh_graph {
   uint32_t* work = nullptr;
   uint32_t* work_lpt = nullptr;  // same lists, classes 1-2 heaviest first (work_lpt(), on demand)
   uint64_t n_work[3] = {0, 0, 0};
+  uint32_t class0_max = 0;  // largest |N+(x)| of class 0 (the warp kernels' staging bound)
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
   eh_graph* sym = nullptr;  // NEXT-2: symmetric (unpruned) trie, built on first use (sym.cu)

@@ -279,6 +279,7 @@ void build_worklists(eh_graph* g) {
   uint64_t lo[3], hi[3];  // class c holds lo[c] <= d < hi[c]
   lo[0] = 2;
   hi[0] = std::max<uint64_t>(2, small_max + 1);
+  g->class0_max = (uint32_t)(hi[0] - 1);
   lo[1] = hi[0];
   hi[1] = std::max<uint64_t>(lo[1], large_min);
   lo[2] = hi[1];
