@@ -16,5 +16,5 @@ timeout 300 python tools/profile_count.py --query pv --reps 1 > $E/pc.log 2>&1 &
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pv -c 2 -o $E/pv_C3 \
   python tools/profile_count.py --query pv --reps 1 > $E/ncu_pv.log 2>&1; echo "ncu pv rc=$?"
 timeout 300 python tools/profile_count.py --config C4 --query k4 --reps 1 > $E/pc.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_k4 -c 2 -o $E/k4_C4 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_k4 -c 4 -o $E/k4_C4 \
   python tools/profile_count.py --config C4 --query k4 --reps 1 > $E/ncu_k4.log 2>&1; echo "ncu k4 rc=$?"
