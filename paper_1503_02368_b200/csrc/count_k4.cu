@@ -20,8 +20,8 @@
 // i.e. |P cap N+(z)| with P = N+(x) cap N+(y), y = x_i, z = x_j, counted 32 w
 // at a time.  |N+(x)| <= 128: one warp per x (rows on 8-lane groups, then 4-lane
 // groups over the <= 4 words of a row); 128 < |N+(x)| <= 1024: one CTA per x
-// (L up to 128 KB of shared memory); larger x (rare): P materialised per warp
-// in global scratch.  COUNT(*) accumulates per lane in u64 (K4 > 2^32 on C4).
+// (L up to 192 KB of shared memory); larger x (rare when pruned; the hubs of the
+// symmetric data): one CTA per row (k_k4_big).  COUNT(*) accumulates per lane in u64 (K4 > 2^32 on C4).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "rows.cuh"
@@ -299,11 +299,23 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
 }
 
 
-// ------------------------------------------- fallback: |N+(x)| > kCMaxD --
+// ------------------------------------------- hub rows: |N+(x)| > kCMaxD --
 // Rows (x, y = x_i) of the big x are flattened into one index space (prefix
-// sums of their row counts) and taken one per warp: P = N+(x) after y cap
-// N+(y) (kU: all of N(x) cap N(y)) materialised in the warp's global scratch,
-// then for z in P: |P after z cap N+(z)| (kU: all of P) by membership probes.
+// sums of their row counts) and taken one per CTA.  The row's
+//   P = N+(x) after y  cap  N+(y)        (kU: all of N(x) cap N(y))
+// is built in order (stream the smaller side, O(1) bitset probe or binary search
+// into the other; block-ordered compaction) in shared memory (global scratch
+// when it could exceed the staging capacity), then every z in P is a warp task
+// (taken from a shared cursor):  |P after z cap N+(z)|  (kU: all of P) by the
+// cheaper of  (a) probing each p into N+(z) (bit test, or binary search of
+// N+(z)) and (b) streaming N+(z) with coalesced loads, each element binary-
+// searched in P on chip -- the min property applied per (x, y, z) (PAPER.md:
+// 164-170, 628-642).  Before this kernel the hub rows probed all of P for every
+// z with global binary searches (|P|^2 log d work): C4 unpruned 14.4 s.
+constexpr int kBigThreads = 512;
+constexpr uint32_t kBigPCap = 8192;   // P staged on chip up to this many elements (32 KB)
+constexpr uint32_t kBigBmMaxWords = 40960;  // P's bitmap on chip for id spaces up to 1.31 M (160 KB)
+
 struct BigPred {
   const uint4* desc;
   const uint32_t* work;
@@ -320,21 +332,35 @@ struct BigEmit {
   }
 };
 
+__device__ __forceinline__ uint32_t lower_bound_gen(const uint32_t* a, uint32_t n, uint32_t e) {
+  uint32_t lo = 0, len = n;  // generic pointer: shared or global
+  while (len > 0) {
+    const uint32_t h = len >> 1;
+    if (a[lo + h] < e) { lo += h + 1; len -= h + 1; } else { len = h; }
+  }
+  return lo;
+}
+
 template <bool kU>
-__global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
-                                                 const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bx,
-                                                 const uint64_t* __restrict__ boff, uint64_t nbig, uint64_t nrows,
-                                                 uint32_t* __restrict__ pscratch, uint32_t pstride,
-                                                 unsigned long long* __restrict__ ctr) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kBigThreads) k_k4_big(const uint4* __restrict__ desc, const uint32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ bs, const uint32_t* __restrict__ bx,
+                                                        const uint64_t* __restrict__ boff, uint64_t nbig, uint64_t nrows,
+                                                        uint32_t* __restrict__ pscratch, uint32_t pstride,
+                                                        unsigned long long* __restrict__ ctr, uint32_t bm_words) {
+  extern __shared__ __align__(16) uint32_t Psm[];  // kBigPCap, then (bm_words > 0) P as a bitmap over all ids
+  uint32_t* bm = Psm + kBigPCap;
+  constexpr int kW = kBigThreads / 32;
+  for (uint32_t t = threadIdx.x; t < bm_words; t += kBigThreads) bm[t] = 0u;
+  __shared__ unsigned long long s_r;
+  __shared__ uint32_t s_wc[kW], s_z;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint32_t* P = pscratch + gw * pstride;
+  uint32_t* Pglob = pscratch + (uint64_t)blockIdx.x * pstride;
   unsigned long long cnt = 0;
   for (;;) {
-    unsigned long long r = 0;
-    if (lane == 0) r = atomicAdd(&ctr[3], 1ull);
-    r = __shfl_sync(kFull, r, 0);
+    if (threadIdx.x == 0) { s_r = atomicAdd(&ctr[3], 1ull); s_z = 0; }
+    __syncthreads();
+    const unsigned long long r = s_r;
     if (r >= nrows) break;
     uint64_t lo = 0, hi = nbig;  // the big x whose rows contain r: last boff[k] <= r
     while (hi - lo > 1) {
@@ -345,25 +371,97 @@ __global__ void __launch_bounds__(128) k_k4_big(const uint4* __restrict__ desc, 
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;
     const uint32_t* xs = col + (uint64_t)dx.x * 4;
-    if (!kU && i + 2 >= d) continue;
-    const SetRef sy = set_of(desc, col, bs, xs[i]);
-    if (sy.len < 2) continue;
+    const uint32_t y = __ldg(xs + i);
+    const SetRef sy = set_of(desc, col, bs, y);
+    const uint32_t a0 = kU ? 0u : i + 1;  // A = xs[a0, d)
+    if (a0 + 1 >= d || sy.len < 2) {      // |P| < 2 for every z
+      __syncthreads();
+      continue;
+    }
+    // P = A cap N(y), in order: stream the smaller side, probe the other
+    const bool stream_a = (d - a0) <= sy.len;
+    const SetRef sx = set_of(desc, col, bs, x);
+    const uint32_t nsrc = stream_a ? d - a0 : sy.len;
+    const uint32_t* src = stream_a ? xs + a0 : sy.list;
+    uint32_t* P = (min(d - a0, sy.len) <= kBigPCap) ? Psm : Pglob;
     uint32_t np = 0;
-    for (uint32_t j0 = kU ? 0 : i + 1; j0 < d; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      const uint32_t e = (j < d) ? xs[j] : 0u;
-      const uint32_t hit = (j < d) ? member(sy, e) : 0u;
-      const unsigned mask = __ballot_sync(kFull, hit);
-      if (hit) P[np + __popc(mask & lt)] = e;
-      np += __popc(mask);
+    for (uint32_t j0 = 0; j0 < nsrc; j0 += kBigThreads) {
+      const uint32_t j = j0 + threadIdx.x;
+      const uint32_t e = (j < nsrc) ? __ldg(src + j) : 0u;
+      // streaming N(y) against all of N(x): keep only the elements of A (after y)
+      const uint32_t hit = (j < nsrc) && (stream_a ? member(sy, e) : ((kU || e > y) && member(sx, e)));
+      const unsigned m = __ballot_sync(kFull, hit);
+      if (lane == 0) s_wc[w] = __popc(m);
+      __syncthreads();
+      uint32_t base = np, tot = 0;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        const uint32_t c = s_wc[q];
+        if (q < w) base += c;
+        tot += c;
+      }
+      if (hit) P[base + __popc(m & lt)] = e;
+      np += tot;
+      __syncthreads();
     }
-    __syncwarp();
-    for (uint32_t t = 0; t < np; ++t) {
-      const SetRef sz = set_of(desc, col, bs, P[t]);
+    if (bm_words) {  // P's bitmap (cleared again after the row)
+      for (uint32_t t = threadIdx.x; t < np; t += kBigThreads) atomicOr(&bm[P[t] >> 5], 1u << (P[t] & 31));
+      __syncthreads();
+    }
+    // z tasks: warp per z from a shared cursor
+    for (;;) {
+      uint32_t k = 0;
+      if (lane == 0) k = atomicAdd(&s_z, 1u);
+      k = __shfl_sync(kFull, k, 0);
+      if (k >= np) break;
+      const uint32_t z = P[k];
+      const SetRef sz = set_of(desc, col, bs, z);
       if (sz.len == 0) continue;
-      for (uint32_t k = (kU ? 0 : t + 1) + lane; k < np; k += 32) cnt += member(sz, P[k]);
+      const uint32_t* T = kU ? P : P + k + 1;  // the part of P that can meet N+(z)
+      const uint32_t nt = kU ? np : np - k - 1;
+      if (nt == 0) continue;
+      const uint32_t lgt = 32 - __clz(nt), lgz = 32 - __clz(sz.len);
+      // costs in element steps: probe each p of T into N(z); stream N(z) against P
+      // (bit test in P's bitmap, else binary search of T); AND N(z)'s bitset chunks
+      // with P's bitmap (every element of P below z misses N+(z), so the whole
+      // bitmap is exact for the pruned nest too)
+      const uint64_t probe_cost = (uint64_t)nt * (sz.bits ? 2u : 2u * lgz);
+      const uint64_t stream_cost = (uint64_t)sz.len * (bm_words ? 1u : lgt);
+      const uint64_t and_cost = (bm_words && sz.bits) ? (uint64_t)(sz.c1 - sz.c0) * 2u : ~0ull;
+      uint32_t c = 0;
+      if (and_cost <= probe_cost && and_cost <= stream_cost) {
+        const uint4* zb = reinterpret_cast<const uint4*>(sz.bits);
+        for (uint32_t ch = sz.c0 + lane; ch < sz.c1; ch += 32) {
+          const uint4 zw = __ldg(zb + (ch - sz.c0));
+          if (4 * ch + 3 < bm_words) {
+            const uint4 pw = reinterpret_cast<const uint4*>(bm)[ch];
+            c += __popc(zw.x & pw.x) + __popc(zw.y & pw.y) + __popc(zw.z & pw.z) + __popc(zw.w & pw.w);
+          } else {
+            const uint32_t zz[4] = {zw.x, zw.y, zw.z, zw.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (4 * ch + q < bm_words) c += __popc(zz[q] & bm[4 * ch + q]);
+          }
+        }
+      } else if (probe_cost <= stream_cost) {
+        for (uint32_t t = lane; t < nt; t += 32) c += member(sz, T[t]);
+      } else if (bm_words) {
+        for (uint32_t t = lane; t < sz.len; t += 32) {
+          const uint32_t e = __ldg(sz.list + t);
+          c += (bm[e >> 5] >> (e & 31)) & 1u;
+        }
+      } else {
+        for (uint32_t t = lane; t < sz.len; t += 32) {
+          const uint32_t e = __ldg(sz.list + t);
+          const uint32_t p = lower_bound_gen(T, nt, e);
+          c += (p < nt && T[p] == e) ? 1u : 0u;
+        }
+      }
+      cnt += c;
     }
-    __syncwarp();
+    __syncthreads();
+    if (bm_words)
+      for (uint32_t t = threadIdx.x; t < np; t += kBigThreads) bm[P[t] >> 5] = 0u;
   }
   cnt = warp_sum(cnt);
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
@@ -412,11 +510,17 @@ uint64_t k4_impl(eh_graph* g) {
       DBuf<uint64_t> boff(g->alloc, nbig + 1), tot(g->alloc, 1);
       scan_exclusive_u32(brows.p, boff.p, nbig, tot.p, g->alloc, s);
       const uint64_t nrows = read_scalar(tot.p, s);
-      const unsigned gb = (unsigned)kSMs * 8;
-      const uint32_t stride = (uint32_t)g->max_dplus;
-      DBuf<uint32_t> scratch(g->alloc, (size_t)gb * 4 * stride);
-      k_k4_big<kU><<<gb, 128, 0, s>>>(g->desc, g->col, g->bs, bx.p, boff.p, nbig, nrows, scratch.p, stride,
-                                      g->d_counter);
+      // P's bitmap over all ids on chip when it fits next to the P list (C2: 32 KB, C4: 80 KB)
+      const uint32_t bm_words = (g->n_act + 127) / 128 * 4 <= kBigBmMaxWords ? (uint32_t)((g->n_act + 127) / 128 * 4) : 0u;
+      const size_t smem = ((size_t)kBigPCap + bm_words) * 4;
+      EH_CUDA(cudaFuncSetAttribute(k_k4_big<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_k4_big<kU>, kBigThreads, smem));
+      const unsigned gb = (unsigned)std::min<uint64_t>(nrows, (uint64_t)kSMs * std::max(1, per_sm));
+      const uint32_t stride = (uint32_t)g->max_dplus;  // |P| <= max |N+(x)|
+      DBuf<uint32_t> scratch(g->alloc, (size_t)gb * stride);
+      k_k4_big<kU><<<gb, kBigThreads, smem, s>>>(g->desc, g->col, g->bs, bx.p, boff.p, nbig, nrows, scratch.p,
+                                                  stride, g->d_counter, bm_words);
       EH_LAUNCH("k_k4_big");
       EH_CUDA(cudaStreamSynchronize(s));  // scratch is released on return
     }
@@ -438,8 +542,7 @@ uint64_t k4_impl(eh_graph* g) {
 uint64_t count_4cliques(eh_graph* g) { return k4_impl<false>(g); }
 
 // NEXT-2: the unpruned 4-clique nest over the symmetric trie = 24 K4.  Hub
-// lists (> 1024) take the generic per-warp fallback, which is slow on skewed
-// graphs (DESIGN.md NEXT-2).
+// lists (> 1024) take the CTA-per-row kernel k_k4_big (DESIGN.md NEXT-2).
 uint64_t count_4cliques_unpruned(eh_graph* g) { return k4_impl<true>(symmetric_trie(g)); }
 
 }  // namespace eh

@@ -140,6 +140,35 @@ def test_k4_unpruned_hub_fallback():
     assert _k4u(*synth.complete(1100))[0] == 24 * comb(1100, 4)
 
 
+def _two_hubs_over_a_path(leaves: int):
+    # hubs h1, h2 (adjacent) both joined to every leaf; a path over the leaves.  The
+    # 4-cliques are exactly {h1, h2, l_i, l_i+1}: K4 = leaves - 1.  The row (h1, h2)
+    # of the unpruned nest has P = all leaves.
+    h1, h2 = leaves, leaves + 1
+    lv = np.arange(leaves, dtype=np.uint32)
+    src = np.concatenate([np.full(leaves, h1, np.uint32), np.full(leaves, h2, np.uint32), lv[:-1], [h1]])
+    dst = np.concatenate([lv, lv, lv[1:], [h2]]).astype(np.uint32)
+    return src.astype(np.uint32), dst
+
+
+@pytest.mark.parametrize("leaves", [3000, 20000])
+def test_k4_unpruned_hub_rows(leaves):
+    # hub rows (|N(x)| > 1024) on the CTA-per-row kernel; with 20000 leaves the row
+    # (h1, h2) has |P| = 20000, above the on-chip staging capacity (global scratch)
+    src, dst = _two_hubs_over_a_path(leaves)
+    u, k = _k4u(src, dst)
+    assert k == leaves - 1 == oracle.count_4cliques(src, dst)
+    assert u == 24 * (leaves - 1)
+
+
+def test_k4_pruned_hub_rows():
+    # pruned nest with |N+(x)| > 1024: K_1100's lowest-rank vertex has 1099 out-neighbours
+    from math import comb
+    with eh.Graph(*synth.complete(1100)) as g:
+        assert g.stats().max_out_degree == 1099
+        assert g.count_4cliques() == comb(1100, 4)
+
+
 @pytest.mark.parametrize("kw", [dict(tau=2), dict(all_uint=True), dict(no_algo=True), dict(bin_large_min=1)])
 def test_k4_unpruned_invariance(kw):
     src, dst = synth.rmat(11, 16, 77)
