@@ -197,29 +197,30 @@ __device__ __forceinline__ uint32_t and4(const uint4 u, const uint4 v) {
   return __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
 }
 
+template <int G = kG>
 __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restrict__ col,
                                             const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X,
                                             const uint32_t* A, uint32_t na, uint32_t gl) {
   uint32_t c = 0;
   if (kd == kProbe) {
-    for (uint32_t j = gl; j < na; j += kG) c += probe_bits(bs, y, A[j]);
+    for (uint32_t j = gl; j < na; j += G) c += probe_bits(bs, y, A[j]);
   } else if (kd == kAnd) {
     const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
     const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
     const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
     const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
     uint32_t k = lo + gl;                                            // absolute chunk index
-    for (; k + kG < hi; k += 2 * kG) {
-      const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + kG - y.c0));
-      c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + kG - xc0]);
+    for (; k + G < hi; k += 2 * G) {
+      const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + G - y.c0));
+      c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + G - xc0]);
     }
     if (k < hi) c += and4(__ldg(yb + (k - y.c0)), xb[k - xc0]);
   } else if (kd == kStream) {
     const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
     const uint32_t nfull = y.len >> 2;
     uint32_t k = gl;
-    for (; k + kG < nfull; k += 2 * kG) {
-      const uint4 v0 = __ldg(yl + k), v1 = __ldg(yl + k + kG);
+    for (; k + G < nfull; k += 2 * G) {
+      const uint4 v0 = __ldg(yl + k), v1 = __ldg(yl + k + G);
       c += X.contains(v0.x) + X.contains(v0.y) + X.contains(v0.z) + X.contains(v0.w);
       c += X.contains(v1.x) + X.contains(v1.y) + X.contains(v1.z) + X.contains(v1.w);
     }
@@ -229,7 +230,7 @@ __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restri
     }
     if (gl < (y.len & 3)) c += X.contains(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + gl));
   } else if (kd == kSearchGlobal) {
-    for (uint32_t j = gl; j < na; j += kG) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
+    for (uint32_t j = gl; j < na; j += G) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
   }
   return c;
 }
@@ -283,19 +284,20 @@ __device__ __forceinline__ uint32_t block_member(const BlockView& bv, const YInf
 // |A cap N+(y)| = |A cap sparse(y)| + |A cap dense(y)|: the sparse part as a uint
 // row, each dense block ANDed with x's staged bitmap chunk (bitset cap bitset,
 // PAPER.md:636) or, when x is hashed, its bits looked up one by one.
+template <int G = kG>
 __device__ __forceinline__ uint32_t grp_row_block(uint8_t kd, const BlockView& bv, const uint32_t* __restrict__ bs,
                                                   const YInfo& y, const XSet& X, const uint32_t* A, uint32_t na,
                                                   uint32_t gl) {
   if (kd == kProbe) {
     uint32_t c = 0;
-    for (uint32_t j = gl; j < na; j += kG) c += block_member(bv, y, A[j]);
+    for (uint32_t j = gl; j < na; j += G) c += block_member(bv, y, A[j]);
     return c;
   }
-  uint32_t c = (kd == kStream || kd == kSearchGlobal) ? grp_row(kd, bv.bcol, bs, y, X, A, na, gl) : 0u;
+  uint32_t c = (kd == kStream || kd == kSearchGlobal) ? grp_row<G>(kd, bv.bcol, bs, y, X, A, na, gl) : 0u;
   const uint32_t nd = y.c0;
   const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
   const uint4* xb = reinterpret_cast<const uint4*>(X.tab);
-  for (uint32_t k = gl; k < nd; k += kG) {
+  for (uint32_t k = gl; k < nd; k += G) {
     const uint32_t cc = __ldg(bv.bcid + y.pool + k);
     const uint4 m = __ldg(bv.bmask + y.pool + k);
     if (X.mode == kBitmap) {
@@ -330,7 +332,7 @@ struct __align__(16) WarpSmem {
 
 // kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
 // N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG>
 __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
   extern __shared__ __align__(16) uint32_t dsm_w[];
   WarpSmem<kMaxD>* sm_all = reinterpret_cast<WarpSmem<kMaxD>*>(dsm_w);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t grp = lane / kG, gl = lane % kG;
+  const uint32_t grp = lane / kWG, gl = lane % kWG;
   WarpSmem<kMaxD>& sm = sm_all[w];
   const unsigned lt = (1u << lane) - 1u;
   unsigned long long cnt = 0;
@@ -381,11 +383,11 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
       }
     }
     __syncwarp();
-    for (uint32_t r = grp; r < nr; r += 32 / kG) {
+    for (uint32_t r = grp; r < nr; r += 32 / kWG) {
       const uint32_t i = sm.ord[r];
-      cnt += kBlock ? grp_row_block(sm.kind[i], bv, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl)
-           : kUnpruned ? grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
-                       : grp_row(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
+      cnt += kBlock ? grp_row_block<kWG>(sm.kind[i], bv, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl)
+           : kUnpruned ? grp_row<kWG>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
+                       : grp_row<kWG>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
-template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB>  // kXCap > 0: compile-time staging capacity
+template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -414,9 +416,9 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
   uint32_t* xs_s = dsm;             // xcap
   uint32_t* tab = dsm + xcap;       // kTabW
   __shared__ unsigned long long s_wi;
-  constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
+  constexpr uint32_t kGroups = kCtaWarps * 32 / kCG;
   const int lane = threadIdx.x & 31;
-  const uint32_t gid = threadIdx.x / kG, gl = threadIdx.x % kG;
+  const uint32_t gid = threadIdx.x / kCG, gl = threadIdx.x % kCG;
   unsigned long long cnt = 0;
   for (;;) {
     if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
@@ -467,10 +469,10 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
                                           : YInfo{0, 0, 0, 0, 0};
       const uint32_t na = kUnpruned ? d : nrows - i;
       if (kBlock) {
-        cnt += grp_row_block(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
+        cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
       } else {
         const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind(y, na, X);
-        cnt += grp_row(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+        cnt += grp_row<kCG>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       }
       i = inext;
       y = ynext;
@@ -521,10 +523,10 @@ __global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __res
   }
 }
 
-template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0>
+template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
-  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB>;
+  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> items;
@@ -577,9 +579,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
 }
 
 
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG>
 void launch_warp(eh_graph* g, uint64_t nsmall) {
-  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB>;
+  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG>;
   const size_t smem = sizeof(WarpSmem<kMaxD>) * kWK_Warps;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -607,6 +609,9 @@ uint64_t count_impl(eh_graph* g) {
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
     if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock>(g, nsmall, nlarge, 0);
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
+    // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
+    // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)
+    else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4>(g, nsmall, nlarge, xcap);
     else launch_cta<4, 2048, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
