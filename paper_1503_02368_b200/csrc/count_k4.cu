@@ -76,11 +76,11 @@ __device__ __forceinline__ LocalHash build_local_hash(uint32_t* keys, uint16_t* 
   return H;
 }
 
-__device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a) {
+__device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a, uint32_t sf16) {
   if (a == 0 || y.len == 0) return kKSkip;
   if (y.c1 > y.c0) return kKProbe;
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kKSearch;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kKSearch;  // sf16: see count_tri.cu row_kind
   return kKStream;
 }
 
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
-                                                          unsigned long long* __restrict__ ctr) {
+                                                          unsigned long long* __restrict__ ctr, uint32_t sf16) {
   extern __shared__ __align__(16) uint32_t dsm_k4w[];
   K4WarpSmem& sm = reinterpret_cast<K4WarpSmem*>(dsm_k4w)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
       sm.yi[i] = y;
-      sm.kind[i] = k4_kind(y, kU ? d : nrows - i);
+      sm.kind[i] = k4_kind(y, kU ? d : nrows - i, sf16);
     }
     __syncwarp();
     uint32_t nr = 0;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
                                                           unsigned long long* __restrict__ ctr, uint32_t dlo,
-                                                          uint32_t cslot) {
+                                                          uint32_t cslot, uint32_t sf16) {
   constexpr int kCHash = 4 * kMaxD;
   extern __shared__ __align__(16) uint32_t dsm_k4c[];
   uint32_t* xs = dsm_k4c;                                   // kMaxD
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      fill_row<kU>(k4_kind(y, kU ? d : nrows - i), col, bs, y, xs, d, i, H, L + i * S, gl);
+      fill_row<kU>(k4_kind(y, kU ? d : nrows - i, sf16), col, bs, y, xs, d, i, H, L + i * S, gl);
       i = inext;
       y = ynext;
     }
@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(kBigThreads) k_k4_big(const uint4* __restrict_
 template <bool kU>
 uint64_t k4_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
+  const uint32_t sf16 = g->n_act > (1ull << 24) ? 64u : 16u;  // C4 K4 7.44 -> 7.39 ms with 16
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 8 * sizeof(unsigned long long), s));
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
   const uint64_t nlarge = g->n_work[2];
@@ -483,7 +484,7 @@ uint64_t k4_impl(eh_graph* g) {
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k0, 4 * 32, sm0));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k0<<<grid, 4 * 32, sm0, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 5u);
+      k0<<<grid, 4 * 32, sm0, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 5u, sf16);
       EH_LAUNCH("k_k4_cta");
     }
     {
@@ -493,7 +494,7 @@ uint64_t k4_impl(eh_graph* g) {
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 8 * 32, sm1));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u);
+      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u, sf16);
       EH_LAUNCH("k_k4_cta");
     }
     if (g->max_dplus > 512) {
@@ -501,7 +502,7 @@ uint64_t k4_impl(eh_graph* g) {
       auto k2 = k_k4_cta<kU, kCMaxD, 16>;
       EH_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-      k2<<<grid, 16 * 32, sm2, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u);
+      k2<<<grid, 16 * 32, sm2, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u, sf16);
       EH_LAUNCH("k_k4_cta");
     }
     if (g->max_dplus > (uint64_t)kCMaxD) {
@@ -529,7 +530,7 @@ uint64_t k4_impl(eh_graph* g) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(K4WarpSmem) * kWWarps;
     EH_CUDA(cudaFuncSetAttribute(k_k4_warp<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_k4_warp<kU><<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter);
+    k_k4_warp<kU><<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter, sf16);
     EH_LAUNCH("k_k4_warp");
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

@@ -134,14 +134,14 @@ __device__ __forceinline__ void fill_x(const XIdx& s, int tid, int nt) {
 // element by element, because every hit must be attributed to its z, and
 // extracting the set bits of ANDed chunks measured slower on B200 than probing
 // (DESIGN.md NEXT-1).  Rows whose bitset span misses x's span are skipped.
-__device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XIdx& X) {
+__device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XIdx& X, uint32_t sf16) {
   if (a == 0 || y.len == 0) return kSkip;
   if (y.c1 > y.c0) {
     if (y.c1 <= (X.amin >> 7) || y.c0 > (X.amax >> 7)) return kSkip;
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kSearch;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearch;  // sf16: see count_tri.cu row_kind
   return kStream;
 }
 
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict
                                                         const uint32_t* __restrict__ col,
                                                         const uint32_t* __restrict__ bs,
                                                         const uint32_t* __restrict__ work, uint64_t nwork,
-                                                        unsigned long long* __restrict__ t,
+                                                        unsigned long long* __restrict__ t, uint32_t sf16,
                                                         unsigned long long* __restrict__ ctr) {
   extern __shared__ __align__(16) uint32_t dsm_pw[];
   PvWarpSmem& sm = reinterpret_cast<PvWarpSmem*>(dsm_pw)[threadIdx.x >> 5];
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict
     bool need_x = false;  // only STREAM rows read x's staged structure
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = yinfo(desc, sm.xs[i]);
-      const uint8_t kd = row_kind(y, nrows - i, X);
+      const uint8_t kd = row_kind(y, nrows - i, X, sf16);
       sm.yi[i] = y;
       sm.kind[i] = kd;
       need_x |= kd == kStream;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restri
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
-                                                          unsigned long long* __restrict__ t,
+                                                          unsigned long long* __restrict__ t, uint32_t sf16,
                                                           unsigned long long* __restrict__ ctr, uint32_t xcap) {
   extern __shared__ __align__(16) uint32_t dsm_pc[];
   uint32_t* xs_s = dsm_pc;                                          // xcap
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restri
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      const uint32_t c = group_sum(pv_row(row_kind(y, nrows - i, X), y, X, i, lc, t, col, bs, gl), lane);
+      const uint32_t c = group_sum(pv_row(row_kind(y, nrows - i, X, sf16), y, X, i, lc, t, col, bs, gl), lane);
       if (gl == 0 && c) {
         if (lc) atomicAdd(&lc[i], c);
         else atomicAdd(&t[xs[i]], (unsigned long long)c);
@@ -395,6 +395,7 @@ __global__ void k_barbell(const uint4* __restrict__ desc, const uint32_t* __rest
 
 void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
   cudaStream_t s = g->stream;
+  const uint32_t sf16 = g->n_act > (1ull << 24) ? 64u : 16u;  // C3 t(v) 15.03 -> 14.79 ms with 16
   const uint64_t n = g->n_act;
   EH_CUDA(cudaMemsetAsync(d_t, 0, std::max<uint64_t>(1, n) * 8, s));
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
@@ -409,7 +410,7 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
     int per_sm = 0;
     EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pv_cta, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t,
+    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t, sf16,
                                                  g->d_counter, xcap);
     EH_LAUNCH("k_pv_cta");
   }
@@ -417,7 +418,7 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWarps - 1) / kWarps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(PvWarpSmem) * kWarps;
     EH_CUDA(cudaFuncSetAttribute(k_pv_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pv_warp<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, g->d_counter);
+    k_pv_warp<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
     EH_LAUNCH("k_pv_warp");
   }
 }

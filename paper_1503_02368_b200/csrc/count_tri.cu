@@ -155,6 +155,13 @@ __device__ __forceinline__ XSet build_xset(uint32_t* tab, uint32_t tab_words, co
 }
 
 // Decide the intersection for row i of x (y = xs[i], |A| = a).
+// sf16: the SEARCH side is taken when |A| log2|B| sf16/16 < |B| (c13).  A binary
+// search costs log2|B| dependent loads, cheap when the lists are L2-resident
+// (narrow graphs: sf16 = 16) and dear when they stream from HBM (above 2^24 active
+// ids, the wide kernels: sf16 = 64; a compile-time constant -- as a runtime value
+// it also changed the wide kernel's code generation, C5 900 -> 1050 ms).  Measured: C3 9.46 -> 9.20 ms, C4 1.52 -> 1.47, C2 0.333 -> 0.318
+// with 16 instead of 64; C5 903 ms with 64 vs 956 with 16.
+template <uint32_t sf16>
 __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XSet& X) {
   if (a == 0 || y.len == 0) return kSkip;
   if (y.c1 > y.c0) {
@@ -167,7 +174,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * 4 < y.len) return kSearchGlobal;
+  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearchGlobal;
   return kStream;
 }
 
@@ -332,7 +339,7 @@ struct __align__(16) WarpSmem {
 
 // kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
 // N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64>
 __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = kBlock ? yinfo_block(bv, sm.xs[i]) : yinfo(desc, sm.xs[i]);
       const uint8_t kd = kBlock ? row_kind_block(y, nrows - i)
-                       : kUnpruned ? row_kind_unpruned(y, d, X) : row_kind(y, nrows - i, X);
+                       : kUnpruned ? row_kind_unpruned(y, d, X) : row_kind<kSF>(y, nrows - i, X);
       sm.yi[i] = y;
       sm.kind[i] = kd;
       need_x |= kBlock || (kd == kAnd || kd == kStream);
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
-template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG>  // kXCap > 0: compile-time staging capacity
+template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG, uint32_t kSF = 64>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
       if (kBlock) {
         cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
       } else {
-        const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind(y, na, X);
+        const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind<kSF>(y, na, X);
         cnt += grp_row<kCG>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       }
       i = inext;
@@ -523,10 +530,10 @@ __global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __res
   }
 }
 
-template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG>
+template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG, uint32_t kSF = 64>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
-  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG>;
+  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG, kSF>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> items;
@@ -579,9 +586,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
 }
 
 
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64>
 void launch_warp(eh_graph* g, uint64_t nsmall) {
-  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG>;
+  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF>;
   const size_t smem = sizeof(WarpSmem<kMaxD>) * kWK_Warps;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -611,13 +618,14 @@ uint64_t count_impl(eh_graph* g) {
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
     // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)
-    else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4>(g, nsmall, nlarge, xcap);
-    else launch_cta<4, 2048, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
+    else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4, 16>(g, nsmall, nlarge, xcap);
+    else launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
     // staging sized for class 0 (|N+(x)| <= 64 by default): 30 KB instead of 43 KB
     // per 8-warp CTA, one more CTA per SM (measured: C3 9.48 -> 9.41 ms)
-    if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 0>(g, nsmall);
+    if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16>(g, nsmall);
+    else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, nsmall);
     else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0>(g, nsmall);
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
