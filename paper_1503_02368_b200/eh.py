@@ -207,7 +207,11 @@ class Graph:
             lib().eh_free(h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: module globals may already be gone
+            pass
 
     def __enter__(self):
         return self

@@ -147,6 +147,20 @@ def test_huge_star_and_hub():
     assert _gpu_counts(s, d, k4=True)[:2] == (199_999, 0)
 
 
+@pytest.mark.parametrize("stride", [256, 512, 1 << 12])
+def test_constant_low_digits(stride):
+    # every id a multiple of `stride`: the canonical keys' low 8 / 9 / 12 bits are
+    # constant, so the first radix pass(es) are skipped as trivial and the fused
+    # canonicalisation runs in a later pass (or, with one distinct key, alone)
+    leaves = (np.arange(1, 301, dtype=np.uint32) * stride).astype(np.uint32)
+    s = np.concatenate([np.zeros(300, np.uint32), leaves[:-1]])
+    d = np.concatenate([leaves, leaves[1:]])
+    _check(s, d)
+    assert _gpu_counts(s, d)[:2] == (299, 0)
+    one = np.full(1000, stride, np.uint32)  # one distinct edge, repeated: every pass trivial
+    assert _gpu_counts(np.zeros(1000, np.uint32), one)[2].m_undirected == 1
+
+
 # ------------------------------------------------------------------ invariances (T5/T6) --
 @pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(block_layout=True),
                                 dict(block_layout=True, tau=2), dict(block_layout=True, bin_large_min=1),
