@@ -204,7 +204,7 @@ __device__ __forceinline__ uint32_t and4(const uint4 u, const uint4 v) {
   return __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
 }
 
-template <int G = kG>
+template <int G = kG, bool kPiv = false>
 __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restrict__ col,
                                             const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X,
                                             const uint32_t* A, uint32_t na, uint32_t gl) {
@@ -237,7 +237,29 @@ __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restri
     }
     if (gl < (y.len & 3)) c += X.contains(__ldg(col + (uint64_t)y.list * 4 + nfull * 4 + gl));
   } else if (kd == kSearchGlobal) {
-    for (uint32_t j = gl; j < na; j += G) c += gmem_search(col + (uint64_t)y.list * 4, y.len, A[j]);
+    const uint32_t* L = col + (uint64_t)y.list * 4;
+    const uint32_t n = y.len;
+    if (kPiv && n >= 4 * G) {
+      // the group's lanes load G-1 pivots (the last element of each of G equal
+      // slices of N+(y)) in one round; every search then starts inside one slice,
+      // log2(G) fewer dependent loads per element of A
+      const uint32_t gbase = (threadIdx.x & 31) & ~(uint32_t)(G - 1);
+      const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << gbase);
+      const uint32_t mine = (gl < G - 1) ? __ldg(L + (uint64_t)(gl + 1) * n / G - 1) : 0u;
+      uint32_t piv[G - 1];
+#pragma unroll
+      for (int q = 0; q < G - 1; ++q) piv[q] = __shfl_sync(gmask, mine, q, G);
+      for (uint32_t j = gl; j < na; j += G) {
+        const uint32_t e = A[j];
+        uint32_t k = 0;
+#pragma unroll
+        for (int q = 0; q < G - 1; ++q) k += (piv[q] < e);
+        const uint32_t lo = (uint32_t)((uint64_t)k * n / G), hi = (uint32_t)((uint64_t)(k + 1) * n / G);
+        c += gmem_search(L + lo, hi - lo, e);
+      }
+    } else {
+      for (uint32_t j = gl; j < na; j += G) c += gmem_search(L, n, A[j]);
+    }
   }
   return c;
 }
@@ -339,7 +361,7 @@ struct __align__(16) WarpSmem {
 
 // kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
 // N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false>
 __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
@@ -394,7 +416,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
       const uint32_t i = sm.ord[r];
       cnt += kBlock ? grp_row_block<kWG>(sm.kind[i], bv, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl)
            : kUnpruned ? grp_row<kWG>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
-                       : grp_row<kWG>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
+                       : grp_row<kWG, kPiv>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -406,7 +428,8 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
-template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG, uint32_t kSF = 64>  // kXCap > 0: compile-time staging capacity
+template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG, uint32_t kSF = 64,
+          bool kPiv = false>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -479,7 +502,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
         cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
       } else {
         const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind<kSF>(y, na, X);
-        cnt += grp_row<kCG>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+        cnt += grp_row<kCG, kPiv && !kUnpruned>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       }
       i = inext;
       y = ynext;
@@ -530,10 +553,11 @@ __global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __res
   }
 }
 
-template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG, uint32_t kSF = 64>
+template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG, uint32_t kSF = 64,
+          bool kPiv = false>
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
-  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG, kSF>;
+  auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG, kSF, kPiv>;
   const size_t smem = (size_t)(xcap + TABW) * 4;
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> items;
@@ -586,9 +610,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
 }
 
 
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false>
 void launch_warp(eh_graph* g, uint64_t nsmall) {
-  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF>;
+  auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF, kPiv>;
   const size_t smem = sizeof(WarpSmem<kMaxD>) * kWK_Warps;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
@@ -614,19 +638,23 @@ uint64_t count_impl(eh_graph* g) {
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
     uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
-    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock>(g, nsmall, nlarge, 0);
-    else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock>(g, nsmall, nlarge, xcap);
+    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
+    else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
     // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)
     else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4, 16>(g, nsmall, nlarge, xcap);
-    else launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16>(g, nsmall, nlarge, xcap);
+    else launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, xcap);
   }
   if (nsmall) {
     // staging sized for class 0 (|N+(x)| <= 64 by default): 30 KB instead of 43 KB
     // per 8-warp CTA, one more CTA per SM (measured: C3 9.48 -> 9.41 ms)
-    if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16>(g, nsmall);
+    // SEARCH rows start inside one of 8 pivot slices on the larger graphs (> 2^20 active
+    // ids; measured C3 9.15 -> 8.92 ms, C5 900 -> 887; slower on C2 / C4)
+    const bool big = g->n_act > (1ull << 20);
+    if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16, true>(g, nsmall);
+    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16>(g, nsmall);
     else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, nsmall);
-    else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0>(g, nsmall);
+    else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall);
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
