@@ -152,6 +152,7 @@ __device__ __forceinline__ void credit(uint32_t* lc, unsigned long long* t, cons
 }
 
 // Row (x, y = xs[i]) on an 8-lane group; returns this lane's hit count.
+template <bool kPiv>
 __device__ __forceinline__ uint32_t pv_row(uint8_t kd, const YInfo& y, const XIdx& X, uint32_t i, uint32_t* lc,
                                            unsigned long long* t, const uint32_t* __restrict__ col,
                                            const uint32_t* __restrict__ bs, uint32_t gl) {
@@ -184,8 +185,26 @@ __device__ __forceinline__ uint32_t pv_row(uint8_t kd, const YInfo& y, const XId
       }
     }
   } else if (kd == kSearch) {
-    for (uint32_t j = i + 1 + gl; j < d; j += kG)
-      if (gmem_search(col + (uint64_t)y.list * 4, y.len, xs[j])) { credit(lc, t, xs, (int)j); ++c; }
+    const uint32_t* L = col + (uint64_t)y.list * 4;
+    const uint32_t n = y.len;
+    if (kPiv && n >= 4 * kG) {  // 7 slice pivots loaded once per row (count_tri.cu grp_row)
+      const unsigned gmask = 0xFFu << ((threadIdx.x & 31) & ~7u);
+      const uint32_t mine = (gl < kG - 1) ? __ldg(L + (uint64_t)(gl + 1) * n / kG - 1) : 0u;
+      uint32_t piv[kG - 1];
+#pragma unroll
+      for (int q = 0; q < kG - 1; ++q) piv[q] = __shfl_sync(gmask, mine, q, kG);
+      for (uint32_t j = i + 1 + gl; j < d; j += kG) {
+        const uint32_t e = xs[j];
+        uint32_t k = 0;
+#pragma unroll
+        for (int q = 0; q < kG - 1; ++q) k += (piv[q] < e);
+        const uint32_t lo = (uint32_t)((uint64_t)k * n / kG), hi = (uint32_t)((uint64_t)(k + 1) * n / kG);
+        if (gmem_search(L + lo, hi - lo, e)) { credit(lc, t, xs, (int)j); ++c; }
+      }
+    } else {
+      for (uint32_t j = i + 1 + gl; j < d; j += kG)
+        if (gmem_search(L, n, xs[j])) { credit(lc, t, xs, (int)j); ++c; }
+    }
   }
   return c;
 }
@@ -208,6 +227,7 @@ struct __align__(16) PvWarpSmem {
   uint8_t ord[kWarpMaxD];
 };
 
+template <bool kPiv>
 __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict__ desc,
                                                         const uint32_t* __restrict__ col,
                                                         const uint32_t* __restrict__ bs,
@@ -259,7 +279,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict
     uint32_t cx = 0;
     for (uint32_t r = grp; r < nr; r += 32 / kG) {
       const uint32_t i = sm.ord[r];
-      const uint32_t c = group_sum(pv_row(sm.kind[i], sm.yi[i], X, i, sm.lc, t, col, bs, gl), lane);
+      const uint32_t c = group_sum(pv_row<kPiv>(sm.kind[i], sm.yi[i], X, i, sm.lc, t, col, bs, gl), lane);
       if (gl == 0 && c) {
         atomicAdd(&sm.lc[i], c);  // y = N+(x)[i] is in every triangle of its row
         cx += c;
@@ -275,6 +295,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict
 }
 
 // ------------------------------------------------------------- CTA kernel --
+template <bool kPiv>
 __global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
@@ -321,7 +342,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restri
     while (i < nrows) {
       const uint32_t inext = i + kGroups;
       const YInfo ynext = (inext < nrows) ? yinfo(desc, xs[inext]) : YInfo{0, 0, 0, 0, 0};
-      const uint32_t c = group_sum(pv_row(row_kind(y, nrows - i, X, sf16), y, X, i, lc, t, col, bs, gl), lane);
+      const uint32_t c = group_sum(pv_row<kPiv>(row_kind(y, nrows - i, X, sf16), y, X, i, lc, t, col, bs, gl), lane);
       if (gl == 0 && c) {
         if (lc) atomicAdd(&lc[i], c);
         else atomicAdd(&t[xs[i]], (unsigned long long)c);
@@ -391,14 +412,9 @@ __global__ void k_barbell(const uint4* __restrict__ desc, const uint32_t* __rest
   if (lane == 0 && (lo | hi)) add_u128_atomic(out2, lo, hi);
 }
 
-}  // namespace
-
-void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
+template <bool kPiv>
+static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
   cudaStream_t s = g->stream;
-  const uint32_t sf16 = g->n_act > (1ull << 24) ? 64u : 16u;  // C3 t(v) 15.03 -> 14.79 ms with 16
-  const uint64_t n = g->n_act;
-  EH_CUDA(cudaMemsetAsync(d_t, 0, std::max<uint64_t>(1, n) * 8, s));
-  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
   const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
   const uint64_t nlarge = g->n_work[1] + g->n_work[2];
   if (nlarge) {
@@ -406,21 +422,35 @@ void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
     while (xcap < g->max_dplus && xcap < kCtaXCapMax) xcap *= 2;
     if (const char* e = getenv("EH_PV_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: forces the unstaged path
     const size_t smem = cta_smem(xcap);
-    EH_CUDA(cudaFuncSetAttribute(k_pv_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kc = k_pv_cta<kPiv>;
+    EH_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pv_cta, kCtaWarps * 32, smem));
+    EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-    k_pv_cta<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t, sf16,
-                                                 g->d_counter, xcap);
+    kc<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t, sf16,
+                                           g->d_counter, xcap);
     EH_LAUNCH("k_pv_cta");
   }
   if (nsmall) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWarps - 1) / kWarps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(PvWarpSmem) * kWarps;
-    EH_CUDA(cudaFuncSetAttribute(k_pv_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pv_warp<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
+    auto kw = k_pv_warp<kPiv>;
+    EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kw<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
     EH_LAUNCH("k_pv_warp");
   }
+}
+
+}  // namespace
+
+void triangles_per_vertex(eh_graph* g, unsigned long long* d_t) {
+  cudaStream_t s = g->stream;
+  const uint32_t sf16 = g->n_act > (1ull << 24) ? 64u : 16u;  // C3 t(v) 15.03 -> 14.79 ms with 16
+  EH_CUDA(cudaMemsetAsync(d_t, 0, std::max<uint64_t>(1, g->n_act) * 8, s));
+  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
+  // pivot-started SEARCH rows above 2^20 active ids, as in count_tri.cu
+  if (g->n_act > (1ull << 20)) pv_launch<true>(g, d_t, sf16);
+  else pv_launch<false>(g, d_t, sf16);
 }
 
 void count_lollipop_barbell(eh_graph* g, bool barbell, uint64_t out2[2]) {
