@@ -5,9 +5,10 @@
 // cursor per list), which leaves each list in arbitrary order.  Degree
 // orientation bounds every list: |N+(x)| <= sqrt(2m) (each out-neighbour has
 // degree >= deg(x) >= |N+(x)|), so lists are short and sort in on-chip memory:
-//   len <= 256         one warp, bitonic network in registers, E = 1, 2, 4 or 8
-//                      keys per lane (__shfl_xor_sync across lanes)
-//   257 .. 1024        one warp, bitonic network in shared memory
+//   len <= 32          four segments per warp: 8-, 16- or 32-lane bitonic networks
+//   len <= 1024        one warp, bitonic network in registers, E = 2, 4, 8, 16 or 32
+//                      keys per lane (__shfl_xor_sync across lanes; measured faster than
+//                      the shared-memory network for 257..1024: C3 load 7.98 -> 7.73 ms)
 //   1025 .. 8192       one CTA, bitonic network in shared memory
 //   longer (rare)      gathered as (segment << 32 | value) keys and sorted by the
 //                      device-wide LSD radix sort, then scattered back.
@@ -21,7 +22,7 @@ namespace eh {
 namespace {
 
 constexpr uint32_t kPad = 0xFFFFFFFFu;
-constexpr int kMidMax = 1024, kMidWarps = 8;
+constexpr int kMidMax = 1024;  // register tiers up to here (E = 32 keys per lane)
 constexpr int kBigMax = 8192, kBigThreads = 1024;
 
 struct Seg {
@@ -84,6 +85,61 @@ __global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* 
   }
 }
 
+// Segments of <= 32 keys, four per warp: when the four are all <= 8 keys they
+// are sorted at once by 8-lane bitonic networks, when <= 16 two at a time by
+// 16-lane networks, else one at a time by the whole warp (lists of consecutive
+// ranks have similar lengths, so the branch is nearly always uniform).
+template <int S>
+__device__ __forceinline__ uint32_t subwarp_bitonic(uint32_t x, int lane) {
+  const int sl = lane & (S - 1);
+#pragma unroll
+  for (int k = 2; k <= S; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t o = __shfl_xor_sync(kFull, x, j);
+      const bool lower = (sl & j) == 0, up = (sl & k) == 0;
+      x = (lower == up) ? min(x, o) : max(x, o);
+    }
+  }
+  return x;
+}
+
+template <int S>
+__device__ __forceinline__ void sort_group(uint32_t* __restrict__ data, const Seg& sg, const uint32_t* __restrict__ ids,
+                                           uint64_t t0, uint64_t nids, int lane) {
+  const uint64_t t = t0 + lane / S;  // this lane's segment
+  const int sl = lane & (S - 1);
+  uint32_t n = 0;
+  uint32_t* p = nullptr;
+  if (t < nids) {
+    const uint32_t v = ids[t];
+    n = sg.len[v];
+    p = data + sg.off16[v] * 4;
+  }
+  uint32_t x = ((uint32_t)sl < n) ? p[sl] : kPad;
+  x = subwarp_bitonic<S>(x, lane);
+  if ((uint32_t)sl < n) p[sl] = x;
+}
+
+__global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t t0 = warp * 4; t0 < nids; t0 += nw * 4) {
+    const uint32_t mylen = (lane < 4 && t0 + lane < nids) ? sg.len[ids[t0 + lane]] : 0u;
+    const uint32_t mx = __reduce_max_sync(kFull, mylen);
+    if (mx <= 8) {
+      sort_group<8>(data, sg, ids, t0, nids, lane);
+    } else if (mx <= 16) {
+      sort_group<16>(data, sg, ids, t0, nids, lane);
+      sort_group<16>(data, sg, ids, t0 + 2, nids, lane);
+    } else {
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) sort_group<32>(data, sg, ids, t0 + q, nids, lane);
+    }
+  }
+}
+
 // Bitonic sort of s[0..N) (N power of two) by `nt` cooperating threads.
 template <bool kCta>
 __device__ __forceinline__ void bitonic_smem(uint32_t* s, uint32_t N, uint32_t tid, uint32_t nt) {
@@ -98,27 +154,6 @@ __device__ __forceinline__ void bitonic_smem(uint32_t* s, uint32_t N, uint32_t t
       }
       if (kCta) __syncthreads(); else __syncwarp();
     }
-  }
-}
-
-__global__ void __launch_bounds__(kMidWarps * 32) k_seg_mid(uint32_t* __restrict__ data, Seg sg,
-                                                              const uint32_t* __restrict__ ids, uint64_t nids) {
-  __shared__ uint32_t sm[kMidWarps][kMidMax];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t warp = (uint64_t)blockIdx.x * kMidWarps + w;
-  const uint64_t nw = (uint64_t)gridDim.x * kMidWarps;
-  uint32_t* s = sm[w];
-  for (uint64_t t = warp; t < nids; t += nw) {
-    const uint32_t v = ids[t];
-    const uint32_t n = sg.len[v];
-    uint32_t* p = data + sg.off16[v] * 4;
-    uint32_t N = 64;
-    while (N < n) N <<= 1;
-    for (uint32_t i = lane; i < N; i += 32) s[i] = (i < n) ? p[i] : kPad;
-    __syncwarp();
-    bitonic_smem<false>(s, N, lane, 32);
-    for (uint32_t i = lane; i < n; i += 32) p[i] = s[i];
-    __syncwarp();
   }
 }
 
@@ -181,23 +216,22 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
   if (nseg == 0 || max_len <= 1) return;
   const Seg sg{off16, len};
   DBuf<uint32_t> ids(al, nseg);
-  const uint32_t bounds[7][2] = {{2, 32}, {33, 64}, {65, 128}, {129, 256}, {257, (uint32_t)kMidMax},
+  const uint32_t bounds[8][2] = {{2, 32}, {33, 64}, {65, 128}, {129, 256}, {257, 512}, {513, (uint32_t)kMidMax},
                                  {(uint32_t)kMidMax + 1, (uint32_t)kBigMax}, {(uint32_t)kBigMax + 1, 0xFFFFFFFFu}};
-  for (int tier = 0; tier < 7; ++tier) {
+  for (int tier = 0; tier < 8; ++tier) {
     if (max_len < bounds[tier][0]) break;
     const uint64_t k = select_if(nseg, LenPred{len, bounds[tier][0], bounds[tier][1]}, IdEmit{ids.p}, al, s);
     if (k == 0) continue;
-    if (tier <= 3) {
+    if (tier <= 5) {
       const unsigned g = grid_for(k * 32, 256);
-      if (tier == 0) k_seg_regs<1><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      if (tier == 0) k_seg_small<<<grid_for(k * 8, 256), 256, 0, s>>>(data, sg, ids.p, k);
       else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, ids.p, k);
       else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, ids.p, k);
-      else k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      else k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, ids.p, k);
       EH_LAUNCH("k_seg_regs");
-    } else if (tier == 4) {
-      k_seg_mid<<<grid_for(k, kMidWarps), kMidWarps * 32, 0, s>>>(data, sg, ids.p, k);
-      EH_LAUNCH("k_seg_mid");
-    } else if (tier == 5) {
+    } else if (tier == 6) {
       k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, ids.p, k);
       EH_LAUNCH("k_seg_big");
     } else {
