@@ -182,6 +182,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
 // (hubs on both sides), so the choice uses explicit costs: PROBE a bit tests,
 // STREAM |N(y)| lookups in x's structure (log2 d when it is the sorted list),
 // SEARCH a binary searches of N(y), AND as above.
+template <uint32_t sf16>
 __device__ __forceinline__ uint8_t row_kind_unpruned(const YInfo& y, uint32_t a, const XSet& X) {
   if (a == 0 || y.len == 0) return kSkip;
   const uint32_t lgx = (X.mode == kSorted) ? (32 - __clz(X.d)) : 1u;
@@ -195,8 +196,8 @@ __device__ __forceinline__ uint8_t row_kind_unpruned(const YInfo& y, uint32_t a,
     }
     return (stream < a) ? kStream : kProbe;
   }
-  const uint64_t search = (uint64_t)a * (32 - __clz(y.len)) * 4;
-  return (y.c0 != kNoAlgo && search < stream) ? kSearchGlobal : kStream;
+  const uint64_t search = (uint64_t)a * (32 - __clz(y.len)) * sf16;
+  return (y.c0 != kNoAlgo && search < stream * 16) ? kSearchGlobal : kStream;
 }
 
 // ---- group-level row bodies: kG lanes, gl = lane within the group --------
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
     for (uint32_t i = lane; i < nrows; i += 32) {
       const YInfo y = kBlock ? yinfo_block(bv, sm.xs[i]) : yinfo(desc, sm.xs[i]);
       const uint8_t kd = kBlock ? row_kind_block(y, nrows - i)
-                       : kUnpruned ? row_kind_unpruned(y, d, X) : row_kind<kSF>(y, nrows - i, X);
+                       : kUnpruned ? row_kind_unpruned<kSF>(y, d, X) : row_kind<kSF>(y, nrows - i, X);
       sm.yi[i] = y;
       sm.kind[i] = kd;
       need_x |= kBlock || (kd == kAnd || kd == kStream);
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
       if (kBlock) {
         cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
       } else {
-        const uint8_t kd = kUnpruned ? row_kind_unpruned(y, na, X) : row_kind<kSF>(y, na, X);
+        const uint8_t kd = kUnpruned ? row_kind_unpruned<kSF>(y, na, X) : row_kind<kSF>(y, na, X);
         cnt += grp_row<kCG, kPiv && !kUnpruned>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       }
       i = inext;
@@ -644,7 +645,11 @@ uint64_t count_impl(eh_graph* g) {
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
     uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
     if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
-    if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
+    // the unpruned nest takes the wide shapes on every graph; its SEARCH factor still
+    // follows the graph size (L2-resident lists: C3 unpruned 415.6 -> 386.9 ms)
+    if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096)
+      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, 0);
+    else if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
     // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)
@@ -660,6 +665,7 @@ uint64_t count_impl(eh_graph* g) {
     if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16, true>(g, nsmall);
     else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 0, kG, 16>(g, nsmall);
     else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, nsmall);
+    else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, nsmall);
     else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall);
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
