@@ -51,6 +51,17 @@ extern std::atomic<unsigned long long> g_launches;
    ::eh::check_cuda(cudaGetLastError(), what, __FILE__, __LINE__))
 
 // Device allocator: the caller's hooks (e.g. torch's caching allocator) or cudaMallocAsync.
+// Default device allocation path (no allocator hook): cudaMallocAsync on the
+// handle's stream, with a process-wide cache of large blocks (>= 4 MB, sizes
+// rounded to 2 MB) reused by exact size across loads -- at C5 scale (10.7 GB key
+// buffers) the stream-ordered pool alone re-maps memory on later loads, with single
+// cudaMallocAsync calls blocking for up to 1.8 s.  A cached block carries an event
+// recorded at its release; a new user waits on it (stream order is preserved
+// across streams).  Cache size is bounded; on allocation failure it is flushed and
+// the allocation retried once.  (alloc.cu)
+void* block_cache_alloc(size_t bytes, cudaStream_t stream);
+void block_cache_free(void* p, cudaStream_t stream);
+
 struct Allocator {
   void* (*hook_alloc)(size_t, void*, void*) = nullptr;
   void (*hook_free)(void*, void*, void*) = nullptr;
@@ -65,19 +76,14 @@ struct Allocator {
       p = hook_alloc(bytes, (void*)stream, ctx);
       if (!p) fail(EH_ENOMEM, "allocator hook returned NULL for %zu bytes", bytes);
     } else {
-      cudaError_t e = cudaMallocAsync(&p, bytes, stream);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        fail(e == cudaErrorMemoryAllocation ? EH_ENOMEM : EH_ECUDA, "cudaMallocAsync(%zu): %s", bytes,
-             cudaGetErrorString(e));
-      }
+      p = block_cache_alloc(bytes, stream);
     }
     return p;
   }
   void release(void* p) {
     if (!p) return;
     if (hook_free) hook_free(p, (void*)stream, ctx);
-    else cudaFreeAsync(p, stream);
+    else block_cache_free(p, stream);
   }
 };
 
