@@ -161,6 +161,27 @@ def test_constant_low_digits(stride):
     assert _gpu_counts(np.zeros(1000, np.uint32), one)[2].m_undirected == 1
 
 
+def test_block_cache_reuse_across_streams():
+    # the default allocation path caches large blocks (>= 4 MB) across loads; a block
+    # released on one stream and reused on another must wait for the first stream's
+    # work (event-ordered): alternate loads / counts between two streams and a
+    # library-owned one, and free the handles in a different order than they were made
+    import torch
+    src, dst = synth.rmat(16, 16, 31)   # 1 M input edges: 8 MB key buffers
+    ref = oracle.count_triangles(src, dst)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    live = []
+    for r in range(6):
+        st = (s1, s2, None)[r % 3]
+        g = eh.Graph(src, dst, stream=st) if st is not None else eh.Graph(src, dst)
+        assert g.count_triangles() == ref
+        live.append(g)
+        if len(live) == 2:
+            live.pop(0).close()
+    for g in live:
+        g.close()
+
+
 # ------------------------------------------------------------------ invariances (T5/T6) --
 @pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(block_layout=True),
                                 dict(block_layout=True, tau=2), dict(block_layout=True, bin_large_min=1),
