@@ -81,7 +81,8 @@ void* raw_alloc(size_t bytes, cudaStream_t stream) {
 }  // namespace
 
 void* block_cache_alloc(size_t bytes, cudaStream_t stream) {
-  if (bytes < kCacheMin || getenv("EH_NO_BLOCK_CACHE")) return raw_alloc(bytes, stream);
+  static const bool off = getenv("EH_NO_BLOCK_CACHE") != nullptr;  // ablation switch
+  if (bytes < kCacheMin || off) return raw_alloc(bytes, stream);
   bytes = (bytes + kCacheGran - 1) / kCacheGran * kCacheGran;
   int dev = 0;
   EH_CUDA(cudaGetDevice(&dev));

@@ -337,7 +337,8 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t be
   // Measured (tools/radix_bench.cu, B200): C3 keys (44 bits) 8-bit/4096 4.07 ms,
   // 9-bit/8192 3.95 ms; C5 keys (52 bits) 8-bit 110 / 92 ms (4096 / 8192), 9-bit/8192 88.7 ms.
   uint32_t bits = ((span + 8) / 9 < (span + 7) / 8) ? 9u : 8u;
-  if (const char* e = getenv("EH_RADIX_BITS")) bits = (atoi(e) == 9) ? 9u : 8u;
+  static const int bits_env = [] { const char* e = getenv("EH_RADIX_BITS"); return e ? atoi(e) : 0; }();
+  if (bits_env == 8 || bits_env == 9) bits = (uint32_t)bits_env;  // tuning override
   const uint32_t nd = 1u << bits;
   const uint32_t passes = (span + bits - 1) / bits;
   if (passes > (uint32_t)kRMaxPasses) fail(EH_EINVAL, "radix sort: %u key bits", span);
