@@ -115,4 +115,89 @@ uint64_t select_if(uint64_t n, Pred pred, Emit emit, Allocator& al, cudaStream_t
   return read_scalar(tot.p, s);
 }
 
+// ---------------------------------------------------------- partition_k --
+// Stable multi-way partition: klass(i) in [0, C) or -1 (dropped) for i in [0, n);
+// emit(c, pos, i) with pos the rank of i among the selected indices of class c.
+// One count pass (per-tile class counts, class-major), ONE exclusive scan of the
+// C x tiles counts, one emit pass, one host read of the C totals -- instead of C
+// select_if calls with a host synchronisation each.
+constexpr int kPartMaxC = 8;
+
+template <int C, class Klass>
+__global__ void __launch_bounds__(kSelBlock) k_part_count(uint64_t n, Klass klass, uint64_t ntiles,
+                                                          uint64_t* __restrict__ cnt) {
+  __shared__ uint32_t sc[C];
+  if (threadIdx.x < C) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kSelTile + (uint64_t)threadIdx.x * kSelItems;
+  uint32_t mine[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) mine[c] = 0;
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    if (base + k >= n) break;
+    const int c = klass(base + k);
+#pragma unroll
+    for (int q = 0; q < C; ++q) mine[q] += (c == q);
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const uint32_t v = warp_sum(mine[c]);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[c], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < C) cnt[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = sc[threadIdx.x];
+}
+
+template <int C, class Klass, class Emit>
+__global__ void __launch_bounds__(kSelBlock) k_part_emit(uint64_t n, Klass klass, Emit emit, uint64_t ntiles,
+                                                         const uint64_t* __restrict__ off) {
+  __shared__ uint64_t sw[kSelBlock / 32 + 1];
+  const uint64_t base = (uint64_t)blockIdx.x * kSelTile + (uint64_t)threadIdx.x * kSelItems;
+  int cls[kSelItems];
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) cls[k] = (base + k < n) ? klass(base + k) : -1;
+#pragma unroll 1
+  for (int c = 0; c < C; ++c) {
+    uint64_t m = 0;
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k) m += (cls[k] == c);
+    uint64_t tot;
+    uint64_t pos = block_exclusive_scan<kSelBlock>(m, sw, &tot) + off[(uint64_t)c * ntiles + blockIdx.x];
+    if (m) {
+#pragma unroll
+      for (int k = 0; k < kSelItems; ++k)
+        if (cls[k] == c) emit(c, pos++, base + k);
+    }
+  }
+}
+
+template <int C>
+__global__ void k_part_starts(const uint64_t* __restrict__ off, const uint64_t* __restrict__ total, uint64_t ntiles,
+                              uint64_t* __restrict__ starts) {
+  const int c = threadIdx.x;
+  if (c < C) starts[c] = off[(uint64_t)c * ntiles];
+  if (c == C) starts[C] = *total;
+}
+
+// The positions are global: class c's indices land in [starts[c], starts[c+1]) of
+// one output (class-major, each class in index order).  Returns starts[0..C].
+template <int C, class Klass, class Emit>
+void partition_k(uint64_t n, Klass klass, Emit emit, uint64_t starts[C + 1], Allocator& al, cudaStream_t s) {
+  static_assert(C <= kPartMaxC, "classes");
+  for (int c = 0; c <= C; ++c) starts[c] = 0;
+  if (n == 0) return;
+  const uint64_t nt = (n + kSelTile - 1) / kSelTile;
+  DBuf<uint64_t> cnt(al, (size_t)C * nt), off(al, (size_t)C * nt), st(al, C + 2);
+  k_part_count<C, Klass><<<(unsigned)nt, kSelBlock, 0, s>>>(n, klass, nt, cnt.p);
+  EH_LAUNCH("k_part_count");
+  scan_exclusive_u64(cnt.p, off.p, (uint64_t)C * nt, st.p + C + 1, al, s);
+  k_part_emit<C, Klass, Emit><<<(unsigned)nt, kSelBlock, 0, s>>>(n, klass, emit, nt, off.p);
+  EH_LAUNCH("k_part_emit");
+  k_part_starts<C><<<1, 32, 0, s>>>(off.p, st.p + C + 1, nt, st.p);
+  EH_LAUNCH("k_part_starts");
+  EH_CUDA(cudaMemcpyAsync(starts, st.p, (C + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace eh

@@ -194,14 +194,25 @@ __global__ void k_seg_scatter(uint32_t* __restrict__ data, Seg sg, const uint32_
   }
 }
 
-struct LenPred {
+// tier of a segment by its length (-1: nothing to sort), tiers as in segmented_sort_u32
+struct TierOf {
   const uint32_t* len;
-  uint32_t lo, hi;  // lo <= len <= hi
-  __device__ bool operator()(uint64_t v) const { const uint32_t n = len[v]; return n >= lo && n <= hi; }
+  __device__ int operator()(uint64_t v) const {
+    const uint32_t n = len[v];
+    if (n < 2) return -1;
+    if (n <= 32) return 0;
+    if (n <= 64) return 1;
+    if (n <= 128) return 2;
+    if (n <= 256) return 3;
+    if (n <= 512) return 4;
+    if (n <= (uint32_t)kMidMax) return 5;
+    if (n <= (uint32_t)kBigMax) return 6;
+    return 7;
+  }
 };
-struct IdEmit {
+struct TierEmit {
   uint32_t* out;
-  __device__ void operator()(uint64_t pos, uint64_t v) const { out[pos] = (uint32_t)v; }
+  __device__ void operator()(int, uint64_t pos, uint64_t v) const { out[pos] = (uint32_t)v; }
 };
 __global__ void k_gather_len(const uint32_t* __restrict__ len, const uint32_t* __restrict__ ids, uint64_t n,
                              uint32_t* __restrict__ out) {
@@ -215,38 +226,38 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
                         Allocator& al, cudaStream_t s) {
   if (nseg == 0 || max_len <= 1) return;
   const Seg sg{off16, len};
-  DBuf<uint32_t> ids(al, nseg);
-  const uint32_t bounds[8][2] = {{2, 32}, {33, 64}, {65, 128}, {129, 256}, {257, 512}, {513, (uint32_t)kMidMax},
-                                 {(uint32_t)kMidMax + 1, (uint32_t)kBigMax}, {(uint32_t)kBigMax + 1, 0xFFFFFFFFu}};
+  DBuf<uint32_t> all_ids(al, nseg);
+  uint64_t starts[9];  // one partition of the segments by tier (one host synchronisation)
+  partition_k<8>(nseg, TierOf{len}, TierEmit{all_ids.p}, starts, al, s);
   for (int tier = 0; tier < 8; ++tier) {
-    if (max_len < bounds[tier][0]) break;
-    const uint64_t k = select_if(nseg, LenPred{len, bounds[tier][0], bounds[tier][1]}, IdEmit{ids.p}, al, s);
+    const uint64_t k = starts[tier + 1] - starts[tier];
     if (k == 0) continue;
+    const uint32_t* tier_ids = all_ids.p + starts[tier];
     if (tier <= 5) {
       const unsigned g = grid_for(k * 32, 256);
-      if (tier == 0) k_seg_small<<<grid_for(k * 8, 256), 256, 0, s>>>(data, sg, ids.p, k);
-      else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, ids.p, k);
-      else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, ids.p, k);
-      else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, ids.p, k);
-      else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, ids.p, k);
-      else k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, ids.p, k);
+      if (tier == 0) k_seg_small<<<grid_for(k * 8, 256), 256, 0, s>>>(data, sg, tier_ids, k);
+      else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
+      else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
+      else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
+      else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
+      else k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
       EH_LAUNCH("k_seg_regs");
     } else if (tier == 6) {
-      k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, ids.p, k);
+      k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, tier_ids, k);
       EH_LAUNCH("k_seg_big");
     } else {
       DBuf<uint32_t> lens(al, k);
       DBuf<uint64_t> goff(al, k), tot(al, 1);
-      k_gather_len<<<grid_for(k, 256), 256, 0, s>>>(len, ids.p, k, lens.p);
+      k_gather_len<<<grid_for(k, 256), 256, 0, s>>>(len, tier_ids, k, lens.p);
       EH_LAUNCH("k_gather_len");
       scan_exclusive_u32(lens.p, goff.p, k, tot.p, al, s);
       const uint64_t total = read_scalar(tot.p, s);
       DBuf<uint64_t> keys(al, total), alt(al, total);
       const unsigned g = (unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 4);
-      k_seg_gather<<<g, 512, 0, s>>>(data, sg, ids.p, k, goff.p, keys.p);
+      k_seg_gather<<<g, 512, 0, s>>>(data, sg, tier_ids, k, goff.p, keys.p);
       EH_LAUNCH("k_seg_gather");
       uint64_t* sorted = radix_sort_u64(keys.p, alt.p, total, 32 + bitlen(k - 1), al, s);
-      k_seg_scatter<<<g, 512, 0, s>>>(data, sg, ids.p, k, goff.p, sorted);
+      k_seg_scatter<<<g, 512, 0, s>>>(data, sg, tier_ids, k, goff.p, sorted);
       EH_LAUNCH("k_seg_scatter");
     }
   }

@@ -96,14 +96,17 @@ __global__ void k_stats(const uint4* __restrict__ desc, const uint32_t* __restri
 }
 
 // Work lists: vertices with |N+(x)| >= 2 (others close no triangle) by class.
-struct WorkPred {
+struct WorkClass {  // 0: 2 <= d < h0, 1: h0 <= d < h1, 2: d >= h1 (and d >= 2); -1: d < 2
   const uint4* desc;
-  uint32_t lo, hi;  // lo <= d < hi (hi unbounded if open)
-  bool open;
-  __device__ bool operator()(uint64_t v) const {
+  uint32_t h0, h1;
+  __device__ int operator()(uint64_t v) const {
     const uint32_t d = desc[v].y;
-    return d >= lo && (open || d < hi);
+    return d < 2 ? -1 : d < h0 ? 0 : d < h1 ? 1 : 2;
   }
+};
+struct WorkEmit3 {
+  uint32_t* out;
+  __device__ void operator()(int, uint64_t pos, uint64_t v) const { out[pos] = (uint32_t)v; }
 };
 struct WorkEmit {
   uint32_t* out;
@@ -284,16 +287,11 @@ void build_worklists(eh_graph* g) {
   hi[1] = std::max<uint64_t>(lo[1], large_min);
   lo[2] = hi[1];
   hi[2] = 1ull << 33;
-  uint64_t pos = 0;
-  for (int c = 0; c < 3; ++c) {
-    const uint32_t l = (uint32_t)std::min<uint64_t>(lo[c], 0xFFFFFFFFull);
-    const uint32_t h = (uint32_t)std::min<uint64_t>(hi[c], 0xFFFFFFFFull);
-    const uint64_t k = (n == 0 || lo[c] >= hi[c]) ? 0
-                       : select_if(n, WorkPred{g->desc, l, h, hi[c] > 0xFFFFFFFFull},
-                                   WorkEmit{g->work + pos}, al, s);
-    g->n_work[c] = k;
-    pos += k;
-  }
+  // one stable 3-way partition (class-major, each class in rank order)
+  uint64_t starts[4];
+  partition_k<3>(n, WorkClass{g->desc, (uint32_t)hi[0], (uint32_t)std::min<uint64_t>(hi[1], 0xFFFFFFFFull)},
+                 WorkEmit3{g->work}, starts, al, s);
+  for (int c = 0; c < 3; ++c) g->n_work[c] = starts[c + 1] - starts[c];
 }
 
 // The work lists with classes 1 and 2 each in descending-d order (heaviest x
