@@ -297,6 +297,22 @@ __global__ void k_desc_base(const uint64_t* __restrict__ off16, const uint32_t* 
   }
 }
 
+// max and number of non-zero entries (n_act = ids with a neighbour)
+__global__ void k_deg_stats(const uint32_t* __restrict__ a, uint64_t n, unsigned long long* __restrict__ out) {
+  uint32_t mx = 0, nz = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = a[i];
+    mx = max(mx, v);
+    nz += (v != 0);
+  }
+  mx = __reduce_max_sync(kFull, mx);
+  nz = __reduce_add_sync(kFull, nz);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out[0], (unsigned long long)mx);
+    if (nz) atomicAdd(&out[1], (unsigned long long)nz);
+  }
+}
+
 __global__ void k_max_u32(const uint32_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ out) {
   uint32_t mx = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -428,20 +444,21 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   // ---- a4: degree + (degree, id) rank
   DBuf<uint32_t> deg(al, n_ids);
   EH_CUDA(cudaMemsetAsync(deg.p, 0, n_ids * 4, s));
-  DBuf<unsigned long long> dm(al, 2);  // {m, max degree}
-  EH_CUDA(cudaMemsetAsync(dm.p, 0, 16, s));
+  DBuf<unsigned long long> dm(al, 3);  // {m, max degree, n_act}: one host read
+  EH_CUDA(cudaMemsetAsync(dm.p, 0, 24, s));
   if (nk) {
     k_degree<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, deg.p, dm.p);
     EH_LAUNCH("k_degree");
   }
-  k_max_u32<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, reinterpret_cast<uint32_t*>(dm.p + 1));
-  EH_LAUNCH("k_max_u32");
-  unsigned long long hm[2];
-  EH_CUDA(cudaMemcpyAsync(hm, dm.p, 16, cudaMemcpyDeviceToHost, s));
+  k_deg_stats<<<grid_for(n_ids, TB * 8), TB, 0, s>>>(deg.p, n_ids, dm.p + 1);
+  EH_LAUNCH("k_deg_stats");
+  unsigned long long hm[3];
+  EH_CUDA(cudaMemcpyAsync(hm, dm.p, 24, cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   m = hm[0];
   g->m = m;
   const uint32_t max_deg = (uint32_t)hm[1];
+  const uint64_t n_act = hm[2];
   // NEXT-4: the primary rank key of the chosen node ordering (default: degree)
   DBuf<uint64_t> prim;
   uint32_t pbits = bitlen(max_deg);
@@ -470,7 +487,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   }
   DBuf<uint64_t> rkeys(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m))),
       ralt(al, std::max<uint64_t>(1, std::min<uint64_t>(n_ids, 2 * m)));
-  const uint64_t n_act = select_if(n_ids, ActivePred{deg.p}, RankKeyEmit{prim.p, deg.p, b, rkeys.p}, al, s);
+  select_emit(n_ids, ActivePred{deg.p}, RankKeyEmit{prim.p, deg.p, b, rkeys.p}, al, s);  // n_act known
   g->n_act = n_act;
   // select_if emits the ids in ascending order and LSD radix passes are stable:
   // sorting by the primary bits alone gives the (primary, id) order
@@ -501,7 +518,17 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   k_pad4<<<grid_for(n_act, TB * 4), TB, 0, s>>>(dplus.p, n_act, p4.p);
   EH_LAUNCH("k_pad4");
   scan_exclusive_u32(p4.p, off16.p, n_act, tot.p, al, s);
-  const uint64_t total16 = read_scalar(tot.p, s);
+  // max |N+(x)| depends only on dplus: read it with the padded total (one host read)
+  DBuf<unsigned long long> totmax(al, 2);
+  EH_CUDA(cudaMemsetAsync(totmax.p, 0, 16, s));
+  EH_CUDA(cudaMemcpyAsync(totmax.p, tot.p, 8, cudaMemcpyDeviceToDevice, s));
+  k_max_u32<<<grid_for(n_act, TB * 8), TB, 0, s>>>(dplus.p, n_act, reinterpret_cast<uint32_t*>(totmax.p + 1));
+  EH_LAUNCH("k_max_u32");
+  unsigned long long htm[2];
+  EH_CUDA(cudaMemcpyAsync(htm, totmax.p, 16, cudaMemcpyDeviceToHost, s));
+  EH_CUDA(cudaStreamSynchronize(s));
+  const uint64_t total16 = htm[0];
+  g->max_dplus = htm[1];
   if (total16 >= (1ull << 32)) fail(EH_EINVAL, "graph too large: %llu padded 16-B list blocks", (unsigned long long)total16);
   g->col_elems = total16 * 4;
   g->col = (uint32_t*)g->own(std::max<uint64_t>(16, total16 * 16));
@@ -513,10 +540,6 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
     EH_LAUNCH("k_scatter_col");
   }
   deg.reset();
-  EH_CUDA(cudaMemsetAsync(dmax.p, 0, 4, s));
-  k_max_u32<<<grid_for(n_act, TB * 8), TB, 0, s>>>(dplus.p, n_act, dmax.p);
-  EH_LAUNCH("k_max_u32");
-  g->max_dplus = read_scalar(dmax.p, s);
   mark("scatter");
   segmented_sort_u32(g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s);
   mark("segsort");

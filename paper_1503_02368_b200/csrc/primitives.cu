@@ -354,9 +354,14 @@ static K* radix_impl(K* keys, K* alt, uint64_t n, uint32_t key_bits, uint32_t be
   EH_LAUNCH("k_radix_hist");
   k_radix_base<<<passes, kRMaxDigits, 0, s>>>(hist.p, base.p, trivial.p, n, nd);
   EH_LAUNCH("k_radix_base");
-  uint32_t triv[kRMaxPasses];
-  EH_CUDA(cudaMemcpyAsync(triv, trivial.p, sizeof triv, cudaMemcpyDeviceToHost, s));
-  EH_CUDA(cudaStreamSynchronize(s));
+  // Skipping a pass whose digit is constant needs the flags on the host (one
+  // synchronisation); small sorts just run every pass (a constant-digit pass is
+  // an exact stable copy).
+  uint32_t triv[kRMaxPasses] = {0};
+  if (n >= (1ull << 22)) {
+    EH_CUDA(cudaMemcpyAsync(triv, trivial.p, sizeof triv, cudaMemcpyDeviceToHost, s));
+    EH_CUDA(cudaStreamSynchronize(s));
+  }
   // tile shape (threads x keys per thread); EH_RADIX_CFG selects one for tuning
   static const int cfg_env = [] { const char* e = getenv("EH_RADIX_CFG"); return e ? atoi(e) : -1; }();
   const int cfg = (cfg_env >= 0 && cfg_env <= 3) ? cfg_env

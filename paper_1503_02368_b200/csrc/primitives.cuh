@@ -115,6 +115,19 @@ uint64_t select_if(uint64_t n, Pred pred, Emit emit, Allocator& al, cudaStream_t
   return read_scalar(tot.p, s);
 }
 
+// select_if when the caller already knows the count: no host synchronisation.
+template <class Pred, class Emit>
+void select_emit(uint64_t n, Pred pred, Emit emit, Allocator& al, cudaStream_t s) {
+  if (n == 0) return;
+  const uint64_t nt = (n + kSelTile - 1) / kSelTile;
+  DBuf<uint64_t> cnt(al, nt), tot(al, 1);
+  k_select_count<Pred><<<(unsigned)nt, kSelBlock, 0, s>>>(n, pred, cnt.p);
+  EH_LAUNCH("k_select_count");
+  scan_exclusive_u64(cnt.p, cnt.p, nt, tot.p, al, s);
+  k_select_emit<Pred, Emit><<<(unsigned)nt, kSelBlock, 0, s>>>(n, pred, emit, cnt.p);
+  EH_LAUNCH("k_select_emit");
+}
+
 // ---------------------------------------------------------- partition_k --
 // Stable multi-way partition: klass(i) in [0, C) or -1 (dropped) for i in [0, n);
 // emit(c, pos, i) with pos the rank of i among the selected indices of class c.
@@ -182,20 +195,30 @@ __global__ void k_part_starts(const uint64_t* __restrict__ off, const uint64_t* 
 
 // The positions are global: class c's indices land in [starts[c], starts[c+1]) of
 // one output (class-major, each class in index order).  Returns starts[0..C].
+// Device-side variant: d_starts (C + 2 entries, caller-owned) receives starts[0..C]
+// on the stream; no host synchronisation.
 template <int C, class Klass, class Emit>
-void partition_k(uint64_t n, Klass klass, Emit emit, uint64_t starts[C + 1], Allocator& al, cudaStream_t s) {
+void partition_k_async(uint64_t n, Klass klass, Emit emit, uint64_t* d_starts, Allocator& al, cudaStream_t s) {
   static_assert(C <= kPartMaxC, "classes");
-  for (int c = 0; c <= C; ++c) starts[c] = 0;
-  if (n == 0) return;
+  if (n == 0) {
+    EH_CUDA(cudaMemsetAsync(d_starts, 0, (C + 2) * sizeof(uint64_t), s));
+    return;
+  }
   const uint64_t nt = (n + kSelTile - 1) / kSelTile;
-  DBuf<uint64_t> cnt(al, (size_t)C * nt), off(al, (size_t)C * nt), st(al, C + 2);
+  DBuf<uint64_t> cnt(al, (size_t)C * nt), off(al, (size_t)C * nt);
   k_part_count<C, Klass><<<(unsigned)nt, kSelBlock, 0, s>>>(n, klass, nt, cnt.p);
   EH_LAUNCH("k_part_count");
-  scan_exclusive_u64(cnt.p, off.p, (uint64_t)C * nt, st.p + C + 1, al, s);
+  scan_exclusive_u64(cnt.p, off.p, (uint64_t)C * nt, d_starts + C + 1, al, s);
   k_part_emit<C, Klass, Emit><<<(unsigned)nt, kSelBlock, 0, s>>>(n, klass, emit, nt, off.p);
   EH_LAUNCH("k_part_emit");
-  k_part_starts<C><<<1, 32, 0, s>>>(off.p, st.p + C + 1, nt, st.p);
+  k_part_starts<C><<<1, 32, 0, s>>>(off.p, d_starts + C + 1, nt, d_starts);
   EH_LAUNCH("k_part_starts");
+}
+
+template <int C, class Klass, class Emit>
+void partition_k(uint64_t n, Klass klass, Emit emit, uint64_t starts[C + 1], Allocator& al, cudaStream_t s) {
+  DBuf<uint64_t> st(al, C + 2);
+  partition_k_async<C>(n, klass, emit, st.p, al, s);
   EH_CUDA(cudaMemcpyAsync(starts, st.p, (C + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
 }

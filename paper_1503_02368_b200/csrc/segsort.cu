@@ -62,7 +62,10 @@ __device__ __forceinline__ void warp_bitonic_regs(uint32_t (&x)[E], int lane) {
 }
 
 template <int E>
-__global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
+__global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ all_ids,
+                           const uint64_t* __restrict__ rng) {
+  const uint32_t* ids = all_ids + rng[0];
+  const uint64_t nids = rng[1] - rng[0];
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -121,7 +124,10 @@ __device__ __forceinline__ void sort_group(uint32_t* __restrict__ data, const Se
   if ((uint32_t)sl < n) p[sl] = x;
 }
 
-__global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids, uint64_t nids) {
+__global__ void k_seg_small(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ all_ids,
+                            const uint64_t* __restrict__ rng) {
+  const uint32_t* ids = all_ids + rng[0];
+  const uint64_t nids = rng[1] - rng[0];
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -158,7 +164,10 @@ __device__ __forceinline__ void bitonic_smem(uint32_t* s, uint32_t N, uint32_t t
 }
 
 __global__ void __launch_bounds__(kBigThreads) k_seg_big(uint32_t* __restrict__ data, Seg sg,
-                                                          const uint32_t* __restrict__ ids, uint64_t nids) {
+                                                          const uint32_t* __restrict__ all_ids,
+                                                          const uint64_t* __restrict__ rng) {
+  const uint32_t* ids = all_ids + rng[0];
+  const uint64_t nids = rng[1] - rng[0];
   __shared__ uint32_t s[kBigMax];
   for (uint64_t t = blockIdx.x; t < nids; t += gridDim.x) {
     const uint32_t v = ids[t];
@@ -227,25 +236,32 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
   if (nseg == 0 || max_len <= 1) return;
   const Seg sg{off16, len};
   DBuf<uint32_t> all_ids(al, nseg);
-  uint64_t starts[9];  // one partition of the segments by tier (one host synchronisation)
-  partition_k<8>(nseg, TierOf{len}, TierEmit{all_ids.p}, starts, al, s);
-  for (int tier = 0; tier < 8; ++tier) {
-    const uint64_t k = starts[tier + 1] - starts[tier];
-    if (k == 0) continue;
-    const uint32_t* tier_ids = all_ids.p + starts[tier];
-    if (tier <= 5) {
-      const unsigned g = grid_for(k * 32, 256);
-      if (tier == 0) k_seg_small<<<grid_for(k * 8, 256), 256, 0, s>>>(data, sg, tier_ids, k);
-      else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
-      else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
-      else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
-      else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
-      else k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, tier_ids, k);
-      EH_LAUNCH("k_seg_regs");
-    } else if (tier == 6) {
-      k_seg_big<<<(unsigned)std::min<uint64_t>(k, (uint64_t)kSMs * 2), kBigThreads, 0, s>>>(data, sg, tier_ids, k);
-      EH_LAUNCH("k_seg_big");
-    } else {
+  DBuf<uint64_t> starts(al, 10);  // one partition of the segments by tier, kept on the device:
+  partition_k_async<8>(nseg, TierOf{len}, TierEmit{all_ids.p}, starts.p, al, s);  // no host sync
+  // the tier kernels read their range from `starts`; grids are sized for the worst
+  // case the host knows (nseg, max_len) and stride over what is there
+  const uint32_t tier_min[8] = {2, 33, 65, 129, 257, 513, (uint32_t)kMidMax + 1, (uint32_t)kBigMax + 1};
+  for (int tier = 0; tier < 7; ++tier) {
+    if (max_len < tier_min[tier]) break;
+    const uint64_t* rng = starts.p + tier;
+    const uint64_t kmax = std::min<uint64_t>(nseg, 1ull << 24);
+    const unsigned g = grid_for(kmax * 32, 256);
+    if (tier == 0) k_seg_small<<<grid_for(kmax * 8, 256), 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else if (tier == 5) k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
+    else k_seg_big<<<(unsigned)kSMs * 2, kBigThreads, 0, s>>>(data, sg, all_ids.p, rng);
+    EH_LAUNCH(tier == 6 ? "k_seg_big" : "k_seg_regs");
+  }
+  if (max_len > (uint32_t)kBigMax) {  // rare: device-wide radix sort of the longest segments
+    uint64_t h[2];
+    EH_CUDA(cudaMemcpyAsync(h, starts.p + 7, 16, cudaMemcpyDeviceToHost, s));
+    EH_CUDA(cudaStreamSynchronize(s));
+    const uint64_t k = h[1] - h[0];
+    if (k) {
+      const uint32_t* tier_ids = all_ids.p + h[0];
       DBuf<uint32_t> lens(al, k);
       DBuf<uint64_t> goff(al, k), tot(al, 1);
       k_gather_len<<<grid_for(k, 256), 256, 0, s>>>(len, tier_ids, k, lens.p);
@@ -259,6 +275,7 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
       uint64_t* sorted = radix_sort_u64(keys.p, alt.p, total, 32 + bitlen(k - 1), al, s);
       k_seg_scatter<<<g, 512, 0, s>>>(data, sg, tier_ids, k, goff.p, sorted);
       EH_LAUNCH("k_seg_scatter");
+      EH_CUDA(cudaStreamSynchronize(s));  // temporaries are released on return
     }
   }
 }
