@@ -21,7 +21,7 @@
 // bitmap plus, per 32-bit word, the position of its first element (positions
 // within a word by popcount), or a hash table with a position per slot, or a
 // binary search of the sorted list.  (No AND rows: see row_kind.)  Tuned on
-// C2-C4 (DESIGN.md NEXT-1): 8-warp CTAs with 28 KB of shared memory, 8 per SM.
+// C2-C4 (DESIGN.md NEXT-1): 8-warp CTAs, staging sized to max |N+(x)| (C3: 20 KB).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "rows.cuh"
@@ -35,8 +35,7 @@ constexpr int kWarpMaxD = 128;       // must equal tri_warp_max_degree(): the wo
 constexpr int kWarpTabWords = 256;   // warp-kernel x structure: bitmap of 8192 ids or 256-slot hash
 constexpr int kWarps = 8;
 constexpr int kCtaWarps = 8;
-constexpr uint32_t kCtaXCapMin = 2048;    // N+(x) staged (and counted locally) up to xcap >= this size:
-constexpr uint32_t kCtaXCapMax = 16384;   // xcap = max |N+(x)| rounded up to a power of two, clamped
+constexpr uint32_t kCtaXCapMax = 16384;   // N+(x) staged and counted locally up to max |N+(x)| rounded to 256, clamped
 constexpr int kCtaTabWords = 2048;   // CTA x structure: bitmap of 65536 ids, or a hash of <= 2048 slots
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -295,8 +294,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_pv_warp(const uint4* __restrict
 }
 
 // ------------------------------------------------------------- CTA kernel --
-template <bool kPiv>
-__global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restrict__ desc,
+template <bool kPiv, int kCW = kCtaWarps>
+__global__ void __launch_bounds__(kCW * 32) k_pv_cta(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
@@ -309,7 +308,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32) k_pv_cta(const uint4* __restri
   uint16_t* pos = reinterpret_cast<uint16_t*>(tab + kCtaTabWords);  // kCtaTabWords
   __shared__ unsigned long long s_wi;
   __shared__ uint32_t s_cx;
-  constexpr uint32_t kGroups = kCtaWarps * 32 / kG;
+  constexpr uint32_t kGroups = kCW * 32 / kG;
   const uint32_t lane = threadIdx.x & 31, gid = threadIdx.x / kG, gl = threadIdx.x % kG;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -418,17 +417,19 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
   const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
   const uint64_t nlarge = g->n_work[1] + g->n_work[2];
   if (nlarge) {
-    uint32_t xcap = kCtaXCapMin;
-    while (xcap < g->max_dplus && xcap < kCtaXCapMax) xcap *= 2;
-    if (const char* e = getenv("EH_PV_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: forces the unstaged path
-    const size_t smem = cta_smem(xcap);
-    auto kc = k_pv_cta<kPiv>;
+    // N+(x) staged up to max |N+(x)| rounded up to 256 (smaller CTAs than a power of
+    // two >= 2048: C3 t(v) 13.89 -> 13.80 ms, C4 2.34 -> 2.27 ms)
+    const uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
+    const uint32_t xc = getenv("EH_PV_XCAP") ? (uint32_t)std::max(128, atoi(getenv("EH_PV_XCAP")))  // test hook:
+                                              : xcap;                                         // the unstaged path
+    const size_t smem = cta_smem(xc);
+    auto kc = k_pv_cta<kPiv>;  // 8 warps (4 / 16 measured slower: C3 17.3 / 16.6 ms)
     EH_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
     kc<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t, sf16,
-                                           g->d_counter, xcap);
+                                           g->d_counter, xc);
     EH_LAUNCH("k_pv_cta");
   }
   if (nsmall) {
