@@ -431,12 +431,42 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
+// ---------------------------------------------- bulk async copy (TMA) --
+// 1-D cp.async.bulk global -> shared, completion tracked by an mbarrier
+// (transaction bytes); one thread arms and issues, every thread waits.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
 // ------------------------------------------------------------- CTA kernel --
 // One CTA per x (classes 1-2); its 8-lane groups take rows round-robin
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
 template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG, uint32_t kSF = 64,
-          bool kPiv = false>  // kXCap > 0: compile-time staging capacity
+          bool kPiv = false, bool kTma = !kUnpruned && !kBlock && kCtaWarps == 16>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -450,13 +480,85 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
   // (hub lists of the symmetric trie would otherwise leave one CTA with 10^5 rows)
   const uint32_t xcap = kXCap > 0 ? (uint32_t)kXCap : xcap_rt;
   extern __shared__ __align__(16) uint32_t dsm[];
-  uint32_t* xs_s = dsm;             // xcap
-  uint32_t* tab = dsm + xcap;       // kTabW
+  uint32_t* xs_s = dsm;                         // xcap (kTma: two buffers)
+  uint32_t* tab = dsm + (kTma ? 2 : 1) * xcap;  // kTabW
   __shared__ unsigned long long s_wi;
   constexpr uint32_t kGroups = kCtaWarps * 32 / kCG;
   const int lane = threadIdx.x & 31;
   const uint32_t gid = threadIdx.x / kCG, gl = threadIdx.x % kCG;
   unsigned long long cnt = 0;
+  if constexpr (kTma) {
+    // the rows of x (as in the loop below)
+    auto rows = [&](const uint32_t* xs, const XSet& X, uint32_t d, uint32_t nrows, uint32_t r0) {
+      uint32_t i = r0 + gid;
+      YInfo y = (i < nrows) ? (kBlock ? yinfo_block(bv, xs[i]) : yinfo(desc, xs[i])) : YInfo{0, 0, 0, 0, 0};
+      while (i < nrows) {
+        const uint32_t inext = i + kGroups;
+        const YInfo ynext = (inext < nrows) ? (kBlock ? yinfo_block(bv, xs[inext]) : yinfo(desc, xs[inext]))
+                                            : YInfo{0, 0, 0, 0, 0};
+        const uint32_t na = kUnpruned ? d : nrows - i;
+        if (kBlock) {
+          cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
+        } else {
+          const uint8_t kd = kUnpruned ? row_kind_unpruned<kSF>(y, na, X) : row_kind<kSF>(y, na, X);
+          cnt += grp_row<kCG, kPiv && !kUnpruned>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+        }
+        i = inext;
+        y = ynext;
+      }
+    };
+    // Pruned set-level nest, wide shape (> 2^24 active ids): N+(x) arrives by TMA
+    // (1-D cp.async.bulk, mbarrier transaction count) into one of two buffers while
+    // the previous x's rows run; thread 0 takes the next work item and issues its
+    // copy at the start of each x.  Measured: C5 887 -> 878 ms; on the narrow
+    // 4-warp shape it is slower (C3 8.90 -> 9.52 ms: thread 0's dependent loads
+    // delay the CTA's next barrier), so that shape keeps plain staged loads.
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    __shared__ uint4 s_dx[2];
+    __shared__ unsigned long long s_wi2[2];
+    auto prefetch = [&](int b) {  // thread 0
+      const unsigned long long w = atomicAdd(&ctr[2], 1ull);
+      s_wi2[b] = w;
+      if (w < nwork) {
+        const uint4 q = __ldg(desc + __ldg(work + w));
+        s_dx[b] = q;
+        if (q.y <= xcap) {
+          const uint32_t bytes = (q.y + 3) / 4 * 16;  // lists are padded to 16 B
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+          mbar_arrive_tx(&s_bar[b], bytes);
+          bulk_g2s(xs_s + (uint32_t)b * xcap, col + (uint64_t)q.x * 4, bytes, &s_bar[b]);
+        } else {
+          mbar_arrive(&s_bar[b]);  // unstaged x: complete the phase without a copy
+        }
+      }
+    };
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      prefetch(0);
+    }
+    __syncthreads();
+    for (uint32_t it = 0;; ++it) {
+      const int cur = it & 1;
+      if (s_wi2[cur] >= nwork) break;
+      const uint4 dx = s_dx[cur];
+      if (threadIdx.x == 0) prefetch(cur ^ 1);
+      const uint32_t d = dx.y;
+      const uint32_t* xs = col + (uint64_t)dx.x * 4;
+      if (d <= xcap) {
+        mbar_wait(&s_bar[cur], (it >> 1) & 1u);  // k-th use of a buffer waits on phase parity k & 1
+        xs = xs_s + (uint32_t)cur * xcap;
+      }
+      const XSet X = build_xset(tab, (d <= xcap) ? (uint32_t)kTabW : 0u, xs, d, threadIdx.x, blockDim.x);
+      __syncthreads();
+      rows(xs, X, d, d - 1, 0u);
+      __syncthreads();
+    }
+    cnt = warp_sum(cnt);
+    if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
+    return;
+  }
   for (;;) {
     if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
     __syncthreads();
@@ -565,7 +667,7 @@ template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0
 void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
   if (XCAP > 0) xcap = XCAP;
   auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG, kSF, kPiv>;
-  const size_t smem = (size_t)(xcap + TABW) * 4;
+  const size_t smem = (size_t)((!kUnpruned && !kBlock && NW == 16 ? 2 : 1) * xcap + TABW) * 4;  // TMA: two buffers
   cudaStream_t s = g->stream;
   DBuf<unsigned long long> items;
   DBuf<uint32_t> hslot, hubk, hub_bm;
@@ -637,7 +739,9 @@ uint64_t count_impl(eh_graph* g) {
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
   // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
   // the symmetric trie's hub lists always take the wide shape (measured: C3 2.70 -> 1.27 s)
-  const bool wide = g->n_act > kWideIds || kUnpruned;
+  // test hook EH_TRI_WIDE: the wide (> 2^24 ids) kernels on any graph, so the tests
+  // reach their TMA staging (and, with EH_TRI_XCAP, its unstaged branch)
+  const bool wide = g->n_act > kWideIds || kUnpruned || getenv("EH_TRI_WIDE") != nullptr;
   const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
   const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
   if (nlarge) {
@@ -649,7 +753,8 @@ uint64_t count_impl(eh_graph* g) {
     // follows the graph size (L2-resident lists: C3 unpruned 415.6 -> 386.9 ms)
     if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096)
       launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, 0);
-    else if (wide && xcap <= 4096) launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
+    else if (wide && xcap <= 4096 && !getenv("EH_TRI_XCAP"))
+      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
     // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)

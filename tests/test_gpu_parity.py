@@ -161,6 +161,22 @@ def test_constant_low_digits(stride):
     assert _gpu_counts(np.zeros(1000, np.uint32), one)[2].m_undirected == 1
 
 
+@pytest.mark.parametrize("xcap", [None, "128"])
+def test_wide_shape_tma_staging(monkeypatch, xcap):
+    # EH_TRI_WIDE (test hook) runs the wide (> 2^24 ids) triangle kernels on a small
+    # graph: N+(x) staged by TMA (cp.async.bulk + mbarrier) double buffering; with
+    # EH_TRI_XCAP=128 the lists above 128 take the unstaged branch (mbarrier phase
+    # completed without a copy)
+    src, dst = synth.rmat(14, 16, 41)
+    ref = oracle.count_triangles(src, dst)
+    monkeypatch.setenv("EH_TRI_WIDE", "1")
+    if xcap:
+        monkeypatch.setenv("EH_TRI_XCAP", xcap)
+    with eh.Graph(src, dst) as g:
+        assert g.stats().max_out_degree > 128
+        assert g.count_triangles() == ref
+
+
 def test_block_cache_reuse_across_streams():
     # the default allocation path caches large blocks (>= 4 MB) across loads; a block
     # released on one stream and reused on another must wait for the first stream's
