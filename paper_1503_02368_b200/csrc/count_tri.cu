@@ -205,12 +205,12 @@ __device__ __forceinline__ uint32_t and4(const uint4 u, const uint4 v) {
   return __popc(u.x & v.x) + __popc(u.y & v.y) + __popc(u.z & v.z) + __popc(u.w & v.w);
 }
 
-template <int G = kG, bool kPiv = false, int kSl = 8>  // kSl: pivot slices (16 measured: C3 +2 %, C5 -0.5 %)
+template <int G = kG, bool kPiv = false, int kSl = 8, int kAndU = 2>  // kSl: pivot slices (16 measured: C3 +2 %, C5 -0.5 %)
 __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restrict__ col,
                                             const uint32_t* __restrict__ bs, const YInfo& y, const XSet& X,
                                             const uint32_t* A, uint32_t na, uint32_t gl) {
   uint32_t c = 0;
-  if (kd == kProbe) {
+  if (kd == kProbe) {  // (4 probes in flight per lane measured slower: C3 8.63 -> 8.75 ms)
     for (uint32_t j = gl; j < na; j += G) c += probe_bits(bs, y, A[j]);
   } else if (kd == kAnd) {
     const uint32_t xc0 = X.lo >> 7, xc1 = xc0 + (X.nbits >> 7);
@@ -218,11 +218,21 @@ __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restri
     const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
     const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
     uint32_t k = lo + gl;                                            // absolute chunk index
-    for (; k + G < hi; k += 2 * G) {
-      const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + G - y.c0));
-      c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + G - xc0]);
+    if (kAndU == 4) {  // 4 chunk loads in flight per lane (narrow shape on large graphs: C3 8.90 -> 8.63 ms)
+      for (; k + 3 * G < hi; k += 4 * G) {
+        const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + G - y.c0));
+        const uint4 u2 = __ldg(yb + (k + 2 * G - y.c0)), u3 = __ldg(yb + (k + 3 * G - y.c0));
+        c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + G - xc0]) + and4(u2, xb[k + 2 * G - xc0]) +
+             and4(u3, xb[k + 3 * G - xc0]);
+      }
+      for (; k < hi; k += G) c += and4(__ldg(yb + (k - y.c0)), xb[k - xc0]);
+    } else {  // 2 in flight (C2, C4, and the wide shape: C5 879 vs 907 ms with 4)
+      for (; k + G < hi; k += 2 * G) {
+        const uint4 u0 = __ldg(yb + (k - y.c0)), u1 = __ldg(yb + (k + G - y.c0));
+        c += and4(u0, xb[k - xc0]) + and4(u1, xb[k + G - xc0]);
+      }
+      if (k < hi) c += and4(__ldg(yb + (k - y.c0)), xb[k - xc0]);
     }
-    if (k < hi) c += and4(__ldg(yb + (k - y.c0)), xb[k - xc0]);
   } else if (kd == kStream) {
     const uint4* yl = reinterpret_cast<const uint4*>(col) + y.list;
     const uint32_t nfull = y.len >> 2;
@@ -368,7 +378,8 @@ struct __align__(16) WarpSmem {
 
 // kUnpruned (NEXT-2, unpruned nest on the symmetric trie): row i intersects all of
 // N(x) with N(y) (no suffix restriction) and every element of N(x) is a row.
-template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false>
+template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false,
+          int kAU = (kPiv && kSF == 16) ? 4 : 2>
 __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4* __restrict__ desc,
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
@@ -423,7 +434,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
       const uint32_t i = sm.ord[r];
       cnt += kBlock ? grp_row_block<kWG>(sm.kind[i], bv, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl)
            : kUnpruned ? grp_row<kWG>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs, d, gl)
-                       : grp_row<kWG, kPiv>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
+                       : grp_row<kWG, kPiv, 8, kAU>(sm.kind[i], col, bs, sm.yi[i], X, sm.xs + i + 1, nrows - i, gl);
     }
     __syncwarp();
   }
@@ -466,7 +477,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // (row i has |A| = d-1-i, so the loads even out), prefetching the next row's
 // descriptor before working on the current one.
 template <int kCtaWarps, int kTabW, int kXCap, bool kUnpruned, bool kBlock, int kMinB, int kCG = kG, uint32_t kSF = 64,
-          bool kPiv = false, bool kTma = !kUnpruned && !kBlock && kCtaWarps == 16>  // kXCap > 0: compile-time staging capacity
+          bool kPiv = false, bool kTma = !kUnpruned && !kBlock && kCtaWarps == 16,
+          int kAU = (kPiv && kCtaWarps == 4) ? 4 : 2>  // kXCap > 0: compile-time staging capacity
 __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* __restrict__ desc,
                                                             const uint32_t* __restrict__ col,
                                                             const uint32_t* __restrict__ bs,
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
           cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
         } else {
           const uint8_t kd = kUnpruned ? row_kind_unpruned<kSF>(y, na, X) : row_kind<kSF>(y, na, X);
-          cnt += grp_row<kCG, kPiv && !kUnpruned>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+          cnt += grp_row<kCG, kPiv && !kUnpruned, 8, kAU>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
         }
         i = inext;
         y = ynext;
@@ -611,7 +623,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
         cnt += grp_row_block<kCG>(row_kind_block(y, na), bv, bs, y, X, xs + i + 1, na, gl);
       } else {
         const uint8_t kd = kUnpruned ? row_kind_unpruned<kSF>(y, na, X) : row_kind<kSF>(y, na, X);
-        cnt += grp_row<kCG, kPiv && !kUnpruned>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
+        cnt += grp_row<kCG, kPiv && !kUnpruned, 8, kAU>(kd, col, bs, y, X, kUnpruned ? xs : xs + i + 1, na, gl);
       }
       i = inext;
       y = ynext;
