@@ -384,7 +384,8 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
                                                              const uint32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ bs,
                                                              const uint32_t* __restrict__ work, uint64_t nwork,
-                                                             unsigned long long* __restrict__ ctr, BlockView bv) {
+                                                             unsigned long long* __restrict__ ctr, BlockView bv,
+                                                             uint32_t cslot) {
   extern __shared__ __align__(16) uint32_t dsm_w[];
   WarpSmem<kMaxD>* sm_all = reinterpret_cast<WarpSmem<kMaxD>*>(dsm_w);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
   unsigned long long cnt = 0;
   for (;;) {
     unsigned long long wi = 0;
-    if (lane == 0) wi = atomicAdd(&ctr[1], 1ull);  // (grabbing 2-8 x per atomic measured no faster)
+    if (lane == 0) wi = atomicAdd(&ctr[cslot], 1ull);  // (grabbing 2-8 x per atomic measured no faster)
     wi = __shfl_sync(kFull, wi, 0);
     if (wi >= nwork) break;
     const uint32_t x = __ldg(work + wi);
@@ -732,7 +733,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
 
 
 template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false>
-void launch_warp(eh_graph* g, uint64_t nsmall) {
+void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, uint32_t cslot = 1) {
+  if (nsmall == 0) return;
+  if (!work) work = g->work;
   auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF, kPiv>;
   const size_t smem = sizeof(WarpSmem<kMaxD>) * kWK_Warps;
   EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -740,15 +743,15 @@ void launch_warp(eh_graph* g, uint64_t nsmall) {
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWK_Warps * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps,
                                                      (uint64_t)kSMs * std::max(1, per_sm));
-  k<<<grid, kWK_Warps * 32, smem, g->stream>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter,
-                                               BlockView{g->bdesc, g->bcol, g->bcid, g->bmask});
+  k<<<grid, kWK_Warps * 32, smem, g->stream>>>(g->desc, g->col, g->bs, work, nsmall, g->d_counter,
+                                               BlockView{g->bdesc, g->bcol, g->bcid, g->bmask}, cslot);
   EH_LAUNCH("k_tri_warp");
 }
 
 template <bool kUnpruned, bool kBlock>
 uint64_t count_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
-  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 4 * sizeof(unsigned long long), s));
+  EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 8 * sizeof(unsigned long long), s));
   // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
   // the symmetric trie's hub lists always take the wide shape (measured: C3 2.70 -> 1.27 s)
   // test hook EH_TRI_WIDE: the wide (> 2^24 ids) kernels on any graph, so the tests
@@ -785,7 +788,10 @@ uint64_t count_impl(eh_graph* g) {
     else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, nsmall);
     else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, nsmall);
     else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, nsmall);
-    else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall);
+    else if (!kUnpruned && !kBlock && g->class0_max <= 64) {  // wide: class 0 with 64-entry staging, min 6 CTAs/SM
+      launch_warp<kUnpruned, kBlock, 64, 6, kG, 64, true>(g, g->n_work[0], g->work, 1u);
+      launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall - g->n_work[0], g->work + g->n_work[0], 6u);
+    } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall);
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
