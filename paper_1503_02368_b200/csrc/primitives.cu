@@ -158,9 +158,11 @@ __global__ void __launch_bounds__(kRMaxDigits) k_radix_base(const unsigned long 
   if (c == n) trivial[p] = 1u;  // every key has this digit: the pass is the identity
 }
 
-// (2) one pass over digits of kBits bits
+// (2) one pass over digits of kBits bits.  Launch bounds: the 8192-key tile is
+// shared-memory-limited to 2 CTAs per SM, so it may use 64 registers (fewer spills
+// of the 16 keys per thread: C3 load 7.38 -> 7.23 ms); the others keep 3 x 512 threads.
 template <typename K, int kBits, int kPBlock, int kRItems, bool kCanon>
-__global__ void __launch_bounds__(kPBlock, 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
+__global__ void __launch_bounds__(kPBlock, (kPBlock == 512 && kRItems == 16) ? 2 : 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
                                                                            K* __restrict__ out, uint64_t n,
                                                                            uint32_t shift,
                                                                            const unsigned long long* __restrict__ base,
