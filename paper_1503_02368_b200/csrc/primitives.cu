@@ -158,11 +158,17 @@ __global__ void __launch_bounds__(kRMaxDigits) k_radix_base(const unsigned long 
   if (c == n) trivial[p] = 1u;  // every key has this digit: the pass is the identity
 }
 
-// (2) one pass over digits of kBits bits.  Launch bounds: the 8192-key tile is
-// shared-memory-limited to 2 CTAs per SM, so it may use 64 registers (fewer spills
-// of the 16 keys per thread: C3 load 7.38 -> 7.23 ms); the others keep 3 x 512 threads.
+// (2) one pass over digits of kBits bits.  Launch bounds at the occupancy the tile's
+// shared memory allows (e.g. the 8192-key u64 tile: 2 CTAs per SM, so 64 registers
+// instead of 40 with 184-B spills: C3 load 7.38 -> 7.23 ms).
+template <int kPBlock, int kRItems, int kKeyBytes>
+constexpr int radix_min_blocks() {  // resident CTAs the shared memory allows (keys + ~8 KB static), <= 1536 threads
+  constexpr int by_smem = (200 * 1024) / (kPBlock * kRItems * kKeyBytes + 8 * 1024);
+  constexpr int by_thr = 3 * 512 / kPBlock;
+  return by_smem < 1 ? 1 : (by_smem < by_thr ? by_smem : by_thr);
+}
 template <typename K, int kBits, int kPBlock, int kRItems, bool kCanon>
-__global__ void __launch_bounds__(kPBlock, (kPBlock == 512 && kRItems == 16) ? 2 : 3 * 512 / kPBlock) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
+__global__ void __launch_bounds__(kPBlock, radix_min_blocks<kPBlock, kRItems, (int)sizeof(K)>()) k_radix_pass(const K* __restrict__ in, CanonSrc cs,
                                                                            K* __restrict__ out, uint64_t n,
                                                                            uint32_t shift,
                                                                            const unsigned long long* __restrict__ base,
