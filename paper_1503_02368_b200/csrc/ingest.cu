@@ -25,8 +25,18 @@ namespace {
 __global__ void k_max_id(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
                          uint32_t* __restrict__ out) {
   uint32_t mx = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    mx = max(mx, max(src[i], dst[i]));
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {  // 128-bit loads
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* d4 = reinterpret_cast<const uint4*>(dst);
+    for (uint64_t i = t0; i < n / 4; i += nt) {
+      const uint4 a = __ldg(s4 + i), b = __ldg(d4 + i);
+      mx = max(mx, max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
+    }
+    done = n / 4 * 4;
+  }
+  for (uint64_t i = done + t0; i < n; i += nt) mx = max(mx, max(src[i], dst[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);

@@ -177,6 +177,18 @@ def test_wide_shape_tma_staging(monkeypatch, xcap):
         assert g.count_triangles() == ref
 
 
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_device_inputs_unaligned(offset):
+    # device-resident inputs that start 4 / 12 bytes past an aligned address: the
+    # id-range pass falls back from 128-bit to 32-bit loads; counts are unchanged
+    import torch
+    src, dst = synth.rmat(13, 16, 61)
+    ts = torch.from_numpy(src.view(np.int32)).cuda()[offset:]
+    td = torch.from_numpy(dst.view(np.int32)).cuda()[offset:]
+    with eh.Graph(ts, td) as g:
+        assert g.count_triangles() == oracle.count_triangles(src[offset:], dst[offset:])
+
+
 def test_block_cache_reuse_across_streams():
     # the default allocation path caches large blocks (>= 4 MB) across loads; a block
     # released on one stream and reused on another must wait for the first stream's
