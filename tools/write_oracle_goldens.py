@@ -8,6 +8,10 @@ committed script that calls only oracle/").  Usage:
 Existing entries for other configs are kept.  With --next1, also the NEXT-1
 values: Lollipop / Barbell COUNT(*) and the sha256 of the
 per-vertex triangle counts t(v) (uint64, in ascending original-id order).
+With --k4, the 4-clique count of every named config (BASELINE.json north star:
+"triangle and 4-clique counts bit-exact with the CPU oracle on all five
+configs"), not only of the 4-clique config C4.  Values already stored for a
+config (four_cliques, next1) are kept unless recomputed.
 """
 import hashlib
 import json
@@ -23,7 +27,7 @@ import synth  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "configs_oracle.json")
 
 
-def main(names, next1=False):
+def main(names, next1=False, k4=False):
     data = json.load(open(OUT)) if os.path.exists(OUT) else {
         "citation": "BASELINE.json configs (SURVEY.md §8 C1..C5); values computed by oracle/eh_oracle.c "
                     "via tools/write_oracle_goldens.py on synthetic inputs from synth/ (DESIGN.md §4)",
@@ -41,7 +45,7 @@ def main(names, next1=False):
                  "max_out_degree": g.max_out_degree, "checksum": str(ck)}
         entry["triangles"] = g.count_triangles()
         t3 = time.time()
-        if cfg.query == "4cliques":
+        if cfg.query == "4cliques" or k4:
             entry["four_cliques"] = g.count_4cliques()
         t4 = time.time()
         entry["oracle_seconds"] = {"generate": round(t1 - t0, 1), "ingest": round(t2 - t1, 1),
@@ -55,13 +59,17 @@ def main(names, next1=False):
                               "seconds": round(time.time() - t4, 1)}
         g.close()
         old = data["configs"].get(name, {})
-        if not next1 and "next1" in old:
-            entry["next1"] = old["next1"]
+        if old.get("checksum") == entry["checksum"]:
+            if "four_cliques" in old and "four_cliques" not in entry:
+                entry["four_cliques"] = old["four_cliques"]
+                entry["oracle_seconds"]["four_cliques"] = old.get("oracle_seconds", {}).get("four_cliques", 0.0)
+            if "next1" in old and "next1" not in entry:
+                entry["next1"] = old["next1"]
         data["configs"][name] = entry
         json.dump(data, open(OUT, "w"), indent=1)
         print(name, entry, flush=True)
 
 
 if __name__ == "__main__":
-    args = [a for a in sys.argv[1:] if a != "--next1"]
-    main(args or ["C1", "C2", "C3", "C4"], next1="--next1" in sys.argv)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(args or ["C1", "C2", "C3", "C4"], next1="--next1" in sys.argv, k4="--k4" in sys.argv)
