@@ -43,7 +43,8 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [vp, ctypes.c_int]
             f.restype = ctypes.c_uint64
-        for name in ("oracle_count_triangles_range", "oracle_count_4cliques_range"):
+        for name in ("oracle_count_triangles_range", "oracle_count_4cliques_range",
+                     "oracle_count_triangles_rank_range", "oracle_count_4cliques_rank_range"):
             f = getattr(lib, name)
             f.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
             f.restype = ctypes.c_uint64
@@ -51,6 +52,8 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [vp, ctypes.c_int]
             f.restype = ctypes.c_uint64
+        lib.oracle_rank_ids.argtypes = [vp, u32p]
+        lib.oracle_rank_ids.restype = ctypes.c_int
         lib.oracle_triangles_at.argtypes = [vp, ctypes.c_uint32]
         lib.oracle_triangles_at.restype = ctypes.c_uint64
         lib.oracle_intersect.argtypes = [u32p, ctypes.c_uint64, u32p, ctypes.c_uint64, u32p]
@@ -117,6 +120,28 @@ class Graph:
 
     def count_4cliques_range(self, x0: int, x1: int, threads: int | None = None) -> int:
         return int(_load().oracle_count_4cliques_range(self._h, x0, x1, threads or default_threads()))
+
+    def _rank_range(self, fn, r0: int, r1: int, threads):
+        r = int(fn(self._h, r0, r1, threads or default_threads()))
+        if r == 2**64 - 1:
+            raise MemoryError("oracle allocation failed")
+        return r
+
+    def count_triangles_rank_range(self, r0: int, r1: int, threads: int | None = None) -> int:
+        """Triangles whose earliest vertex has a rank in [r0, r1) of the ascending
+        (degree, original id) order (eh_oracle.c "Rank ranges")."""
+        return self._rank_range(_load().oracle_count_triangles_rank_range, r0, r1, threads)
+
+    def count_4cliques_rank_range(self, r0: int, r1: int, threads: int | None = None) -> int:
+        """4-cliques whose earliest vertex has a rank in [r0, r1) (eh_oracle.c "Rank ranges")."""
+        return self._rank_range(_load().oracle_count_4cliques_rank_range, r0, r1, threads)
+
+    def rank_ids(self) -> np.ndarray:
+        """Original id of every rank of the (degree, original id) order."""
+        ids = np.empty(max(self.n_vertices, 1), np.uint32)
+        if _load().oracle_rank_ids(self._h, _p32(ids)) != 0:
+            raise MemoryError("oracle allocation failed")
+        return ids[:self.n_vertices]
 
     def count_triangles_unpruned(self, threads: int | None = None) -> int:
         """NEXT-2: the triangle Generic-Join on the symmetric (unpruned) data = 6T."""

@@ -33,6 +33,9 @@
  *            for z in P cap pi_Z Q
  *              K += | P cap Q[z] |          (two scalar merges in total)
  *   COUNT(*) is a uint64 sum ("w:long"; reading c9).
+ *   Rank ranges: both nests with x restricted to the vertices whose rank (their
+ *   position in the order of step 3) lies in [r0, r1) -- sampled outputs for
+ *   sizes where the full count is out of the oracle's reach.
  *   NEXT-1 / NEXT-2: per-vertex counts + Lollipop / Barbell,
  *   and the unpruned nests on the symmetric data -- see their sections below.
  *   intersect (Table `lst:eh_operators`): sorted merge.
@@ -185,10 +188,12 @@ int64_t oracle_intersect(const uint32_t* a, uint64_t na, const uint32_t* b, uint
 #define OUT(g, i) ((g)->adj + (g)->off[i])
 #define DOUT(g, i) ((g)->off[(i) + 1] - (g)->off[i])
 
-/* Triangle loop nest for x in vertex-index range [x0, x1). */
-static uint64_t tri_range(const oracle_graph* g, uint64_t x0, uint64_t x1) {
+/* Triangle loop nest for x in vertex-index range [x0, x1);
+ * with ord != NULL, x runs over ord[x0 .. x1) instead (rank ranges, below). */
+static uint64_t tri_range(const oracle_graph* g, uint64_t x0, uint64_t x1, const uint64_t* ord) {
   uint64_t q = 0;
-  for (uint64_t x = x0; x < x1; ++x) {
+  for (uint64_t p = x0; p < x1; ++p) {
+    const uint64_t x = ord ? ord[p] : p;
     if (DOUT(g, x) == 0) continue;                  /* x in pi_X R cap pi_X T */
     for (uint64_t e = g->off[x]; e < g->off[x + 1]; ++e) {
       const uint64_t y = vindex(g, g->adj[e]);      /* y in R[x] */
@@ -200,9 +205,10 @@ static uint64_t tri_range(const oracle_graph* g, uint64_t x0, uint64_t x1) {
 }
 
 /* 4-clique loop nest for x in [x0, x1), attribute order x, y, z, w. */
-static uint64_t k4_range(const oracle_graph* g, uint64_t x0, uint64_t x1, uint32_t* P) {
+static uint64_t k4_range(const oracle_graph* g, uint64_t x0, uint64_t x1, uint32_t* P, const uint64_t* ord) {
   uint64_t k = 0;
-  for (uint64_t x = x0; x < x1; ++x) {
+  for (uint64_t p = x0; p < x1; ++p) {
+    const uint64_t x = ord ? ord[p] : p;
     if (DOUT(g, x) == 0) continue;
     for (uint64_t e = g->off[x]; e < g->off[x + 1]; ++e) {
       const uint64_t y = vindex(g, g->adj[e]);
@@ -281,6 +287,7 @@ typedef struct {
   volatile uint64_t* next;
   pthread_mutex_t* mu;
   int query; /* 0 = triangles, 1 = 4-cliques, 2 / 3 = the same, unpruned (NEXT-2) */
+  const uint64_t* ord; /* NULL, or the vertex index of each position (rank ranges) */
   uint64_t sum;
   int err;
 } job_t;
@@ -303,8 +310,8 @@ static void* worker(void* arg) {
     pthread_mutex_unlock(j->mu);
     if (a >= j->x1) break;
     const uint64_t b = (a + chunk < j->x1) ? a + chunk : j->x1;
-    j->sum += j->query == 0 ? tri_range(j->g, a, b)
-            : j->query == 1 ? k4_range(j->g, a, b, P)
+    j->sum += j->query == 0 ? tri_range(j->g, a, b, j->ord)
+            : j->query == 1 ? k4_range(j->g, a, b, P, j->ord)
             : j->query == 2 ? tri_unpruned_range(j->g, a, b)
                             : k4_unpruned_range(j->g, a, b, P);
   }
@@ -312,7 +319,8 @@ static void* worker(void* arg) {
   return NULL;
 }
 
-static uint64_t run(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads, int query) {
+static uint64_t run_ord(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads, int query,
+                        const uint64_t* ord) {
   if (!g) return UINT64_MAX;
   if (x1 > g->nv) x1 = g->nv;
   if (x0 >= x1) return 0;
@@ -324,7 +332,7 @@ static uint64_t run(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads
   if (!jobs || !tid) { free(jobs); free(tid); return UINT64_MAX; }
   for (int t = 0; t < threads; ++t) {
     jobs[t].g = g; jobs[t].x0 = x0; jobs[t].x1 = x1; jobs[t].next = &next;
-    jobs[t].mu = &mu; jobs[t].query = query;
+    jobs[t].mu = &mu; jobs[t].query = query; jobs[t].ord = ord;
   }
   for (int t = 1; t < threads; ++t) pthread_create(&tid[t], NULL, worker, &jobs[t]);
   worker(&jobs[0]);
@@ -334,6 +342,10 @@ static uint64_t run(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads
   for (int t = 0; t < threads; ++t) { s += jobs[t].sum; err |= jobs[t].err; }
   free(jobs); free(tid);
   return err ? UINT64_MAX : s;
+}
+
+static uint64_t run(const oracle_graph* g, uint64_t x0, uint64_t x1, int threads, int query) {
+  return run_ord(g, x0, x1, threads, query, NULL);
 }
 
 uint64_t oracle_count_triangles(const oracle_graph* g, int threads) { return run(g, 0, UINT64_MAX, threads, 0); }
@@ -362,7 +374,51 @@ uint64_t oracle_triangles_at(const oracle_graph* g, uint32_t x) {
   const uint32_t* p = (const uint32_t*)bsearch(&x, g->vid, g->nv, sizeof(uint32_t), cmp_u32);
   if (!p) return 0;
   const uint64_t i = (uint64_t)(p - g->vid);
-  return tri_range(g, i, i + 1);
+  return tri_range(g, i, i + 1, NULL);
+}
+
+/*
+ * Rank ranges: the counts restricted to the cliques whose EARLIEST vertex (the
+ * x of the loop nest, PAPER.md:538-542 / 217 on the pruned data) has a rank in
+ * [r0, r1), the rank of a vertex being its position in the total order of step
+ * 3 above -- ascending (degree, original id).  A partition of [0, nv) into
+ * ranges partitions the cliques, so the range counts sum to the full count.
+ * (These are the sampled outputs against which the CUDA path's
+ * eh_count_*_range are checked at sizes where the full oracle count is out of
+ * reach, e.g. 4-cliques of C5.)  UINT64_MAX on allocation failure.
+ */
+static uint64_t* rank_order(const oracle_graph* g) {
+  uint64_t* key = (uint64_t*)malloc((g->nv ? g->nv : 1) * sizeof(uint64_t));
+  if (!key) return NULL;
+  for (uint64_t i = 0; i < g->nv; ++i) key[i] = ((uint64_t)g->deg[i] << 32) | g->vid[i];
+  qsort(key, g->nv, sizeof(uint64_t), cmp_u64);
+  for (uint64_t r = 0; r < g->nv; ++r) key[r] = vindex(g, (uint32_t)key[r]);  /* rank -> vertex index */
+  return key;
+}
+
+static uint64_t rank_range(const oracle_graph* g, uint64_t r0, uint64_t r1, int threads, int query) {
+  if (!g) return UINT64_MAX;
+  uint64_t* ord = rank_order(g);
+  if (!ord) return UINT64_MAX;
+  const uint64_t q = run_ord(g, r0, r1, threads, query, ord);
+  free(ord);
+  return q;
+}
+
+uint64_t oracle_count_triangles_rank_range(const oracle_graph* g, uint64_t r0, uint64_t r1, int threads) {
+  return rank_range(g, r0, r1, threads, 0);
+}
+uint64_t oracle_count_4cliques_rank_range(const oracle_graph* g, uint64_t r0, uint64_t r1, int threads) {
+  return rank_range(g, r0, r1, threads, 1);
+}
+
+/* The original id of every rank (ord[r] = vid of rank r), for tests. */
+int oracle_rank_ids(const oracle_graph* g, uint32_t* ids) {
+  uint64_t* ord = rank_order(g);
+  if (!ord) return -1;
+  for (uint64_t r = 0; r < g->nv; ++r) ids[r] = g->vid[ord[r]];
+  free(ord);
+  return 0;
 }
 
 /*

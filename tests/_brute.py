@@ -84,3 +84,24 @@ def kn_triangles(n: int) -> int:
 
 def kn_4cliques(n: int) -> int:
     return comb(n, 4)
+
+
+def cliques_by_earliest_rank(src, dst, size: int) -> np.ndarray:
+    """Literal definition of the rank-range counts: enumerate every `size`-set
+    whose pairs are all edges (itertools, tiny n only), find its earliest vertex
+    under the (degree, original id) order of SURVEY.md §8(c) step 3, and count
+    it at that vertex's rank (its position in the ascending order).  Returns
+    counts[rank] over the non-isolated vertices."""
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    A = adjacency(src, dst)
+    ids = np.unique(np.concatenate([src, dst]))
+    deg = A.sum(axis=1)
+    active = np.nonzero(deg)[0]
+    order = sorted(active.tolist(), key=lambda i: (int(deg[i]), int(ids[i])))
+    rank = {v: r for r, v in enumerate(order)}
+    out = np.zeros(len(order), dtype=np.int64)
+    for q in itertools.combinations(active.tolist(), size):
+        if all(A[a, b] for a, b in itertools.combinations(q, 2)):
+            out[min(rank[v] for v in q)] += 1
+    return out

@@ -376,3 +376,48 @@ def test_unpruned_rmat_multiples():
         assert g.count_4cliques_unpruned() == 24 * g.count_4cliques()
     finally:
         g.close()
+
+
+# ------------------------------------------------------------ rank ranges --
+def test_w1_rank_ranges(golden_dir):
+    """W1 hand trace: the two triangles are counted at x = r1 and x = r2."""
+    w = json.load(open(os.path.join(golden_dir, "w1_worked_example.json")))
+    g = oracle.Graph(w["src"], w["dst"])
+    n = g.n_vertices
+    assert [g.count_triangles_rank_range(r, r + 1, 1) for r in range(n)] == w["triangles_by_rank"]
+    assert [g.count_4cliques_rank_range(r, r + 1, 1) for r in range(n)] == w["four_cliques_by_rank"]
+    assert g.rank_ids().tolist() == w["rank_ids"]
+    g.close()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 9, 17, 40])
+def test_rank_ranges_kn_closed_form(n):
+    """K_n: every degree is n-1, so rank r is the r-th smallest id and the cliques
+    whose earliest vertex is rank r choose their other members among the n-1-r
+    later ones: C(n-1-r, 2) triangles, C(n-1-r, 3) 4-cliques."""
+    src, dst = synth.complete(n, offset=1000)
+    g = oracle.Graph(src, dst)
+    for r in range(n):
+        assert g.count_triangles_rank_range(r, r + 1, 2) == comb(n - 1 - r, 2)
+        assert g.count_4cliques_rank_range(r, r + 1, 2) == comb(n - 1 - r, 3)
+    assert g.count_4cliques_rank_range(0, n, 3) == comb(n, 4)
+    assert g.count_triangles_rank_range(n, n + 5, 3) == 0
+    g.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_rank_ranges_vs_literal_enumeration(seed):
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(6, 22))
+    src, dst = synth.random_graph(n, int(rng.integers(n, 4 * n)), 900 + seed, id_space=1 << 32)
+    t_ref = B.cliques_by_earliest_rank(src, dst, 3)
+    k_ref = B.cliques_by_earliest_rank(src, dst, 4)
+    g = oracle.Graph(src, dst)
+    nv = g.n_vertices
+    assert nv == t_ref.size
+    assert [g.count_triangles_rank_range(r, r + 1, 2) for r in range(nv)] == t_ref.tolist()
+    assert [g.count_4cliques_rank_range(r, r + 1, 2) for r in range(nv)] == k_ref.tolist()
+    cuts = sorted(set([0, nv] + rng.integers(0, nv + 1, 3).tolist()))
+    assert sum(g.count_4cliques_rank_range(a, b, 3) for a, b in zip(cuts, cuts[1:])) == g.count_4cliques(3)
+    assert sum(g.count_triangles_rank_range(a, b, 3) for a, b in zip(cuts, cuts[1:])) == g.count_triangles(3)
+    g.close()
