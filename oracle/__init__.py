@@ -180,16 +180,18 @@ class Graph:
         """COUNT(*) of Barbell B3,1 on the undirected data."""
         return self._count128(_load().oracle_count_barbell)
 
-    def export(self):
+    def export(self, with_adj: bool = True):
         """(vid, deg, off, adj): sorted original ids, degrees, out-list offsets,
-        out-neighbours (original ids, each list sorted by original id)."""
+        out-neighbours (original ids, each list sorted by original id; None
+        unless with_adj)."""
         nv, m = self.n_vertices, self.m
         vid = np.empty(nv, np.uint32)
         deg = np.empty(nv, np.uint32)
         off = np.empty(nv + 1, np.uint64)
-        adj = np.empty(m, np.uint32)
+        adj = np.empty(m, np.uint32) if with_adj else None
         _load().oracle_export(self._h, _p32(vid), _p32(deg),
-                              off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), _p32(adj))
+                              off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                              _p32(adj) if with_adj else None)
         return vid, deg, off, adj
 
 
