@@ -28,17 +28,31 @@ import synth  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "rank_ranges_oracle.json")
 
 
+BUDGET = 4e11  # per window: sum of |N+(x)|^3 (a bound on the K4 nest's work; C2 measured ~5e9 per s on 8 threads)
+
+
 def windows(dplus: np.ndarray):
+    """Rank windows, each shrunk until its cost proxy sum |N+(x)|^3 fits BUDGET."""
     n = dplus.size
-    w = [(0, min(n, 1 << 16))]
+    c3 = np.concatenate([[0.0], np.cumsum(dplus.astype(np.float64) ** 3)])
+
+    def fwd(a, b):  # [a, b') with b' <= b as large as the budget allows (>= 1 rank)
+        b2 = int(np.searchsorted(c3, c3[a] + BUDGET, side="right")) - 1
+        return a, max(a + 1, min(b, b2))
+
+    def bwd(a, b):  # [a', b) with a' >= a
+        a2 = int(np.searchsorted(c3, c3[b] - BUDGET, side="left"))
+        return min(b - 1, max(a, a2)), b
+
+    w = [fwd(0, min(n, 1 << 16))]
     for f in (0.25, 0.5, 0.75, 0.9):
         a = int(n * f)
-        w.append((a, min(n, a + (1 << 14))))
+        w.append(fwd(a, min(n, a + (1 << 14))))
     rmax = int(np.argmax(dplus))
-    w.append((max(0, rmax - 32), min(n, rmax + 32)))
+    w.append(fwd(max(0, rmax - 4), min(n, rmax + 4)))
     for r in np.argsort(dplus, kind="stable")[::-1][:16].tolist():
         w.append((int(r), int(r) + 1))
-    w.append((max(0, n - 4096), n))
+    w.append(bwd(max(0, n - 4096), n))
     return w
 
 
