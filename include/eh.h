@@ -65,7 +65,12 @@ typedef struct {
    * is tau = 256).  Counts do not depend on tau. */
   uint32_t bitset_tau;
   int32_t device; /* CUDA ordinal, honoured only with EH_SET_DEVICE */
-  void* stream;   /* cudaStream_t used for all work; NULL -> a library-owned stream */
+  /* cudaStream_t used for all work of the handle; NULL -> a library-owned stream
+   * created WITHOUT cudaStreamNonBlocking, i.e. ordered after the work pending on
+   * the legacy default stream.  Ordering contract for EH_INPUT_ON_DEVICE inputs and
+   * device outputs: they must be ready (written) in the order of `stream` -- pass
+   * the stream that produced them, or produce them on the legacy default stream. */
+  void* stream;
   /* Optional device allocator (e.g. the PyTorch caching allocator).  Both or
    * neither must be set.  dev_alloc returning NULL makes the call fail with EH_ENOMEM. */
   void* (*dev_alloc)(size_t bytes, void* stream, void* ctx);
@@ -148,6 +153,36 @@ uint64_t eh_count_triangles(eh_graph* g);
 uint64_t eh_count_4cliques(eh_graph* g);
 
 /*
+ * eh_count_triangles_range / eh_count_4cliques_range -- the same COUNT(*)s
+ * with the outermost attribute x of the loop nest (PAPER.md:538-542 for the
+ * triangle, PAPER.md:217 for the 4-clique, on pruned data every clique is
+ * bound once, at its EARLIEST vertex x) restricted to the ranks [r0, r1).  The
+ * rank of a vertex is its position in the handle's node ordering (the default
+ * EH_ORDER_DEGREE: ascending (degree, original id); rank r has original id
+ * eh_graph_export's orig_id[r]).  Ranks run over [0, n_active); r1 is clamped
+ * to n_active and r0 >= r1 gives 0.  Any partition of [0, n_active) into
+ * ranges partitions the cliques, so the range counts add up to the full count:
+ * this is the unit by which the path shards and the sampled
+ * output the tests check against the CPU oracle where the full oracle count is
+ * out of reach (4-cliques of C5).  The same kernels and launch shapes as the
+ * full counts run over the restricted work lists.  Returns EH_COUNT_ERROR on
+ * error (EH_EINVAL for g == NULL, EH_ENOMEM, EH_ECUDA).
+ */
+uint64_t eh_count_triangles_range(eh_graph* g, uint64_t r0, uint64_t r1);
+uint64_t eh_count_4cliques_range(eh_graph* g, uint64_t r0, uint64_t r1);
+
+/*
+ * eh_alg_bytes_k4 -- B_K4(tau = 32) of SURVEY.md §8(d): the algorithmic bytes
+ * of the 4-clique Generic-Join, B_tri(32) + sum over triangles x < y < z of
+ * bytes_32(N+(z)), bytes_32(S) = 4 |S| for a uint set or 4 x (32-bit words
+ * spanned) for a tau = 32 bitset (the roofline denominator of the K4 bench
+ * line).  Computed on the first call by a statistics kernel (one binary search
+ * per wedge; not part of any count) and cached in the handle.  Returns
+ * EH_COUNT_ERROR on error.
+ */
+uint64_t eh_alg_bytes_k4(eh_graph* g);
+
+/*
  * eh_triangles_per_vertex -- t(v) = the number of triangles containing v, for
  * every non-isolated vertex: the GROUP BY x aggregate
  * of the triangle node of the Lollipop/Barbell GHDs (Example `ex:barbell`,
@@ -188,8 +223,10 @@ uint64_t eh_count_triangles_unpruned(eh_graph* g);
 /*
  * eh_count_4cliques_unpruned -- NEXT-2: the 4-clique Generic-Join on the
  * unpruned (symmetric) data, attribute order x, y, z, w: 24 K4.  Same
- * symmetric trie.  Lists above 1024 elements take a generic per-warp path that
- * is slow on skewed graphs (hub x hub pairs).  Returns EH_COUNT_ERROR on error.
+ * symmetric trie.  Lists above 1024 elements (the hubs) take one CTA per row
+ * (x, y): P = N(x) cap N(y) is built on chip and every z in P picks the
+ * cheapest of probe / stream / bitset AND (DESIGN.md NEXT-2).  Returns
+ * EH_COUNT_ERROR on error.
  */
 uint64_t eh_count_4cliques_unpruned(eh_graph* g);
 
@@ -232,8 +269,18 @@ int eh_graph_stats(const eh_graph* g, eh_stats* out);
  */
 int eh_graph_export(const eh_graph* g, uint64_t* row_ptr, uint32_t* col, uint32_t* orig_id, uint8_t* is_bitset);
 
-/* Release a handle and all its device memory.  NULL-safe. */
+/* Release a handle and all its device memory.  NULL-safe.  With the default
+ * allocation path (no allocator hook) the memory returns to the library's
+ * private pool and its large-block cache, which keep it for the next load
+ * (re-mapping device memory costs ~100 ms per load at C3 size, seconds at C5). */
 void eh_free(eh_graph* g);
+
+/* Give the device memory the library keeps idle (freed large blocks of its
+ * cache, unused memory of its private stream-ordered pools on every device)
+ * back to the driver, e.g. before another allocator needs it.  Waits for the
+ * pending work that last used each block.  Memory of live handles is not
+ * touched.  Also done automatically, once, when a device allocation fails. */
+void eh_release_cached_memory(void);
 
 /* Number of CUDA kernels this library has launched in this process (diagnostics; bench.py). */
 uint64_t eh_launch_count(void);

@@ -1,5 +1,8 @@
-// alloc.cu -- the default device allocation path: cudaMallocAsync plus a
-// process-wide exact-size cache of large blocks (see eh_internal.cuh).
+// alloc.cu -- the default device allocation path: a library-private
+// stream-ordered memory pool per device (cudaMemPoolCreate; the device's default
+// pool, shared with torch / CuPy / ..., is never touched) plus a process-wide
+// exact-size cache of large blocks (see eh_internal.cuh).  Both hold memory
+// until eh_release_cached_memory() (or an allocation failure) gives it back.
 #include "eh_internal.cuh"
 
 #include <map>
@@ -18,11 +21,14 @@ struct Cached {
   cudaEvent_t ev;  // recorded on the releasing stream at release
 };
 
+constexpr int kMaxDev = 64;
+
 struct BlockCache {
   std::mutex mu;
   std::map<std::pair<int, size_t>, std::vector<Cached>> free;  // (device, size) -> idle blocks
   std::unordered_map<void*, std::pair<int, size_t>> big;       // live + idle cached blocks
   size_t idle_bytes = 0, cap = 0;
+  cudaMemPool_t pool[kMaxDev] = {};  // private pools, created on first use
 };
 
 BlockCache& cache() {
@@ -49,18 +55,47 @@ void flush_locked(BlockCache& c, cudaStream_t s) {
   c.idle_bytes = 0;
 }
 
+// The library's pool on device dev (caller holds the lock).  Its release threshold
+// is unbounded: freed memory stays mapped for the next load (re-mapping costs
+// ~100 ms per load at C3 size and up to seconds at C5) until trimmed.
+cudaMemPool_t pool_locked(BlockCache& c, int dev) {
+  if (dev < 0 || dev >= kMaxDev) fail(EH_EINVAL, "device ordinal %d out of range", dev);
+  if (!c.pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p;
+    EH_CUDA(cudaMemPoolCreate(&p, &props));
+    uint64_t thr = UINT64_MAX;
+    EH_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+    c.pool[dev] = p;
+  }
+  return c.pool[dev];
+}
+
+cudaMemPool_t pool_for(int dev) {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  return pool_locked(c, dev);
+}
+
 void* raw_alloc(size_t bytes, cudaStream_t stream) {
   static const bool trace = getenv("EH_ALLOC_TRACE") != nullptr;
   timespec t0, t1;
   if (trace) clock_gettime(CLOCK_MONOTONIC, &t0);
+  int dev = 0;
+  EH_CUDA(cudaGetDevice(&dev));
+  const cudaMemPool_t pool = pool_for(dev);
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
   if (trace) {
     clock_gettime(CLOCK_MONOTONIC, &t1);
     const double ms = (t1.tv_sec - t0.tv_sec) * 1e3 + (t1.tv_nsec - t0.tv_nsec) * 1e-6;
     if (ms > 2.0) fprintf(stderr, "[eh alloc] cudaMallocAsync(%zu) took %.1f ms\n", bytes, ms);
   }
-  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back (to the driver) and retry once
     cudaGetLastError();
     BlockCache& c = cache();
     {
@@ -68,7 +103,8 @@ void* raw_alloc(size_t bytes, cudaStream_t stream) {
       flush_locked(c, stream);
     }
     cudaStreamSynchronize(stream);
-    e = cudaMallocAsync(&p, bytes, stream);
+    cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -126,6 +162,31 @@ void block_cache_free(void* p, cudaStream_t stream) {
   cudaEventRecord(ev, stream);
   c.free[{dev, bytes}].push_back(Cached{p, ev});
   c.idle_bytes += bytes;
+}
+
+void release_cached_memory() {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto& kv : c.free)
+    for (Cached& b : kv.second) {
+      cudaSetDevice(kv.first.first);
+      cudaEventSynchronize(b.ev);  // the last user's work on the block is done
+      cudaFreeAsync(b.p, 0);
+      cudaEventDestroy(b.ev);
+      c.big.erase(b.p);
+    }
+  c.free.clear();
+  c.idle_bytes = 0;
+  for (int d = 0; d < kMaxDev; ++d)
+    if (c.pool[d]) {
+      cudaSetDevice(d);
+      cudaDeviceSynchronize();  // frees still pending in some stream complete first
+      cudaMemPoolTrimTo(c.pool[d], 0);
+    }
+  if (prev >= 0) cudaSetDevice(prev);
+  cudaGetLastError();
 }
 
 }  // namespace eh

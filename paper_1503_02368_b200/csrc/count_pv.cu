@@ -420,7 +420,7 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
     // N+(x) staged up to max |N+(x)| rounded up to 256 (smaller CTAs than a power of
     // two >= 2048: C3 t(v) 13.89 -> 13.80 ms, C4 2.34 -> 2.27 ms)
     const uint32_t xcap = (uint32_t)std::min<uint64_t>(kCtaXCapMax, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
-    const uint32_t xc = getenv("EH_PV_XCAP") ? (uint32_t)std::max(128, atoi(getenv("EH_PV_XCAP")))  // test hook:
+    const uint32_t xc = getenv("EH_TEST_PV_XCAP") ? (uint32_t)std::max(128, atoi(getenv("EH_TEST_PV_XCAP")))  // test hook:
                                               : xcap;                                         // the unstaged path
     const size_t smem = cta_smem(xc);
     auto kc = k_pv_cta<kPiv>;  // 8 warps (4 / 16 measured slower: C3 17.3 / 16.6 ms)

@@ -754,21 +754,21 @@ uint64_t count_impl(eh_graph* g) {
   EH_CUDA(cudaMemsetAsync(g->d_counter, 0, 8 * sizeof(unsigned long long), s));
   // narrow shape: class 0 -> warp kernel, classes 1-2 -> CTA kernel; wide: classes 0-1 -> warp
   // the symmetric trie's hub lists always take the wide shape (measured: C3 2.70 -> 1.27 s)
-  // test hook EH_TRI_WIDE: the wide (> 2^24 ids) kernels on any graph, so the tests
-  // reach their TMA staging (and, with EH_TRI_XCAP, its unstaged branch)
-  const bool wide = g->n_act > kWideIds || kUnpruned || getenv("EH_TRI_WIDE") != nullptr;
+  // test hook EH_TEST_TRI_WIDE: the wide (> 2^24 ids) kernels on any graph, so the tests
+  // reach their TMA staging (and, with EH_TEST_TRI_XCAP, its unstaged branch)
+  const bool wide = g->n_act > kWideIds || kUnpruned || getenv("EH_TEST_TRI_WIDE") != nullptr;
   const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
   const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
   if (nlarge) {
     // unpruned: lists above 4096 use the global hub bitmaps (measured: C3 0.93 -> 0.42 s)
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
     uint32_t xcap = (uint32_t)std::min<uint64_t>(cap, std::max<uint64_t>(256, (g->max_dplus + 255) / 256 * 256));
-    if (const char* e = getenv("EH_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
+    if (const char* e = getenv("EH_TEST_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
     // the unpruned nest takes the wide shapes on every graph; its SEARCH factor still
     // follows the graph size (L2-resident lists: C3 unpruned 415.6 -> 386.9 ms)
     if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096)
       launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, 0);
-    else if (wide && xcap <= 4096 && !getenv("EH_TRI_XCAP"))
+    else if (wide && xcap <= 4096 && !getenv("EH_TEST_TRI_XCAP"))
       launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane

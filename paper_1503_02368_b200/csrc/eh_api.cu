@@ -101,21 +101,15 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       if (c.stream) {
         g->stream = (cudaStream_t)c.stream;
       } else {
-        EH_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        // a BLOCKING stream: it is ordered after the work pending on the legacy default
+        // stream (e.g. torch's default stream writing device-resident inputs)
+        EH_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamDefault));
         g->own_stream = true;
       }
       g->alloc.hook_alloc = c.dev_alloc;
       g->alloc.hook_free = c.dev_free;
       g->alloc.ctx = c.alloc_ctx;
       g->alloc.stream = g->stream;
-      if (!c.dev_alloc) {
-        // keep freed blocks in the stream-ordered pool instead of returning them to
-        // the driver at every synchronisation (re-mapping costs ~100 ms per load)
-        cudaMemPool_t pool;
-        EH_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t thr = UINT64_MAX;
-        EH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-      }
       eh::PhaseTimer timer(g->stream);
       g->d_counter = (unsigned long long*)g->own(8 * sizeof(unsigned long long));
       timer.mark("alloc");
@@ -165,6 +159,33 @@ uint64_t eh_count_4cliques(eh_graph* g) {
     if (!g) eh::fail(EH_EINVAL, "eh_count_4cliques: NULL graph");
     DeviceGuard guard(g->device);
     return eh::count_4cliques(g);
+  });
+}
+
+uint64_t eh_count_triangles_range(eh_graph* g, uint64_t r0, uint64_t r1) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_triangles_range: NULL graph");
+    DeviceGuard guard(g->device);
+    eh::WorkRange range(g, r0, r1);
+    return eh::count_triangles(g);
+  });
+}
+
+uint64_t eh_count_4cliques_range(eh_graph* g, uint64_t r0, uint64_t r1) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_count_4cliques_range: NULL graph");
+    DeviceGuard guard(g->device);
+    eh::work_lpt(g);  // the full LPT order first: the range keeps its sub-order
+    eh::WorkRange range(g, r0, r1);
+    return eh::count_4cliques(g);
+  });
+}
+
+uint64_t eh_alg_bytes_k4(eh_graph* g) {
+  return guarded<uint64_t>(EH_COUNT_ERROR, [&]() -> uint64_t {
+    if (!g) eh::fail(EH_EINVAL, "eh_alg_bytes_k4: NULL graph");
+    DeviceGuard guard(g->device);
+    return eh::alg_bytes_k4(g);
   });
 }
 
@@ -292,6 +313,11 @@ int eh_graph_export(const eh_graph* g, uint64_t* row_ptr, uint32_t* col, uint32_
 }
 
 void eh_free(eh_graph* g) { destroy(g); }
+
+void eh_release_cached_memory(void) {
+  eh::release_cached_memory();
+  ok();
+}
 
 uint64_t eh_launch_count(void) { return eh::g_launches.load(); }
 

@@ -61,6 +61,9 @@ extern std::atomic<unsigned long long> g_launches;
 // the allocation retried once.  (alloc.cu)
 void* block_cache_alloc(size_t bytes, cudaStream_t stream);
 void block_cache_free(void* p, cudaStream_t stream);
+// Give every idle cached block and the unused memory of the private pools back
+// to the driver (eh_release_cached_memory).
+void release_cached_memory();
 
 struct Allocator {
   void* (*hook_alloc)(size_t, void*, void*) = nullptr;
@@ -208,6 +211,7 @@ struct eh_graph {
   uint64_t n_input = 0, m = 0, n_act = 0, max_dplus = 0;
   uint64_t n_bitsets = 0, bs_words = 0, col_elems = 0;
   uint64_t alg_bytes_tri = 0, wedge_work = 0;
+  uint64_t alg_bytes_k4 = 0;  // B_K4(tau = 32), computed on first request (eh_alg_bytes_k4)
 
   // Device trie (rank space).  desc[v] = {col offset in 16-B units, |N+(v)|,
   // bitset pool offset in 16-B chunks (prefix; n_chunks = desc[v+1].z - desc[v].z),
@@ -256,6 +260,23 @@ const uint32_t* work_lpt(eh_graph* g);  // lazy: LPT-ordered work lists (trie.cu
 void compute_stats(eh_graph* g);  // lazy: B_tri, wedge work, #bitset sets
 void build_block_layout(eh_graph* g);  // NEXT-3 composite layout (EH_BLOCK_LAYOUT)
 void build_worklists(eh_graph* g);
+uint64_t alg_bytes_k4(eh_graph* g);  // lazy: B_K4 = B_tri + sum over triangles of bytes(N+(z)) (tau = 32)
+// eh_count_*_range: while alive, the handle's work lists hold only the x with rank in
+// [r0, r1) (class-major, each class and the LPT order preserved); restored on exit.
+class WorkRange {
+ public:
+  WorkRange(eh_graph* g, uint64_t r0, uint64_t r1);
+  ~WorkRange();
+  WorkRange(const WorkRange&) = delete;
+  WorkRange& operator=(const WorkRange&) = delete;
+
+ private:
+  eh_graph* g_;
+  uint32_t* saved_work_;
+  uint32_t* saved_lpt_;
+  uint64_t saved_n_[3];
+  DBuf<uint32_t> work_, lpt_;
+};
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);
 uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept

@@ -417,7 +417,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
 
   // ---- a1-a3: canonical keys, deduplicated.  Default: radix sort over the 2b
-  // significant bits, then unique adjacent keys.  EH_DEDUP=hash selects a fused
+  // significant bits, then unique adjacent keys.  EH_TEST_DEDUP=hash selects a fused
   // canonicalise + GPU hash-set insert (load <= ~0.6) and a compaction of the
   // occupied slots (the downstream steps only need the DISTINCT edges); it was
   // measured slower on C3 (random DRAM sectors, and the unsorted output slows
@@ -425,7 +425,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   uint64_t m = 0, nk = 0;  // nk key entries; m of them are distinct non-loop edges
   DBuf<uint64_t> keys, alt;
   uint64_t* ukeys = nullptr;
-  const char* dd_env = getenv("EH_DEDUP");
+  const char* dd_env = getenv("EH_TEST_DEDUP");
   if (!(dd_env && strcmp(dd_env, "hash") == 0)) {
     keys = DBuf<uint64_t>(al, n);
     alt = DBuf<uint64_t>(al, n);

@@ -124,7 +124,104 @@ __global__ void k_work_unkey(const uint64_t* __restrict__ key, uint64_t n, uint3
     w[k] = (uint32_t)key[k];
 }
 
+// Rank-range restriction of the work lists (eh_count_*_range): position k of a
+// class-major list keeps its class iff the vertex lies in [r0, r1).
+struct RangeClass {
+  const uint32_t* w;
+  uint64_t e0, e1;  // class boundaries (positions)
+  uint32_t r0, r1;
+  __device__ int operator()(uint64_t k) const {
+    const uint32_t v = w[k];
+    if (v < r0 || v >= r1) return -1;
+    return k < e0 ? 0 : k < e1 ? 1 : 2;
+  }
+};
+struct RangeEmit {
+  const uint32_t* w;
+  uint32_t* out;
+  __device__ void operator()(int, uint64_t pos, uint64_t k) const { out[pos] = w[k]; }
+};
+
+// B_K4: sum over triangles x < y < z of bytes(N+(z)) at tau = 32.
+// One warp per x (grid-stride); for each row y = x_i, the lanes take z in
+// N+(x) after y and binary-search N+(y).  Statistics only (not on a count path).
+__global__ void k_k4_bytes(const uint4* __restrict__ desc, const uint32_t* __restrict__ col, uint64_t n_act,
+                           const uint32_t* __restrict__ bytes_tau, unsigned long long* __restrict__ out) {
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned long long acc = 0;
+  for (uint64_t x = warp; x < n_act; x += nwarps) {
+    const uint4 dx = desc[x];
+    const uint32_t* xs = col + (uint64_t)dx.x * 4;
+    for (uint32_t i = 0; i + 1 < dx.y; ++i) {
+      const uint4 dy = desc[xs[i]];
+      if (dy.y == 0) continue;
+      const uint32_t* ys = col + (uint64_t)dy.x * 4;
+      for (uint32_t j = i + 1 + lane; j < dx.y; j += 32) {
+        const uint32_t z = xs[j];
+        uint32_t lo = 0, hi = dy.y;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ys[mid] < z) lo = mid + 1; else hi = mid;
+        }
+        if (lo < dy.y && ys[lo] == z) acc += bytes_tau[z];
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
 }  // namespace
+
+WorkRange::WorkRange(eh_graph* g, uint64_t r0, uint64_t r1) : g_(g) {
+  saved_work_ = g->work;
+  saved_lpt_ = g->work_lpt;
+  for (int c = 0; c < 3; ++c) saved_n_[c] = g->n_work[c];
+  const uint64_t n = saved_n_[0] + saved_n_[1] + saved_n_[2];
+  r1 = std::min<uint64_t>(r1, g->n_act);
+  if (r0 >= r1) r0 = r1 = 0;
+  // the LPT list is filtered too, so the kernels that take it keep their order
+  const uint32_t* lpt = (n && g->work_lpt) ? g->work_lpt : nullptr;
+  work_ = DBuf<uint32_t>(g->alloc, std::max<uint64_t>(1, n));
+  uint64_t starts[4] = {0, 0, 0, 0};
+  partition_k<3>(n, RangeClass{saved_work_, saved_n_[0], saved_n_[0] + saved_n_[1], (uint32_t)r0, (uint32_t)r1},
+                 RangeEmit{saved_work_, work_.p}, starts, g->alloc, g->stream);
+  if (lpt) {
+    lpt_ = DBuf<uint32_t>(g->alloc, std::max<uint64_t>(1, n));
+    partition_k<3>(n, RangeClass{lpt, saved_n_[0], saved_n_[0] + saved_n_[1], (uint32_t)r0, (uint32_t)r1},
+                   RangeEmit{lpt, lpt_.p}, starts, g->alloc, g->stream);
+  }
+  g->work = work_.p;
+  g->work_lpt = lpt ? lpt_.p : nullptr;
+  for (int c = 0; c < 3; ++c) g->n_work[c] = starts[c + 1] - starts[c];
+}
+
+WorkRange::~WorkRange() {
+  cudaStreamSynchronize(g_->stream);  // the filtered lists are released below
+  // a work_lpt() built while restricted belongs to the handle (g->owned) but lists only
+  // the range: it is dropped here (its memory stays with the handle until eh_free)
+  g_->work = saved_work_;
+  g_->work_lpt = saved_lpt_;
+  for (int c = 0; c < 3; ++c) g_->n_work[c] = saved_n_[c];
+}
+
+uint64_t alg_bytes_k4(eh_graph* g) {
+  compute_stats(g);
+  if (g->alg_bytes_k4) return g->alg_bytes_k4;
+  uint64_t tri_z = 0;
+  if (g->n_act) {
+    cudaStream_t s = g->stream;
+    DBuf<unsigned long long> acc(g->alloc, 1);
+    EH_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long), s));
+    k_k4_bytes<<<kSMs * 8, 256, 0, s>>>(g->desc, g->col, g->n_act, g->bytes32, acc.p);
+    EH_LAUNCH("k_k4_bytes");
+    tri_z = read_scalar(reinterpret_cast<const uint64_t*>(acc.p), s);
+  }
+  g->alg_bytes_k4 = g->alg_bytes_tri + tri_z;
+  return g->alg_bytes_k4;
+}
 
 void build_layouts(eh_graph* g) {
   Allocator& al = g->alloc;

@@ -69,8 +69,11 @@ def lib():
         L.eh_count_triangles.restype = u64
         L.eh_count_4cliques.argtypes = [vp]
         L.eh_count_4cliques.restype = u64
-        for name in ("eh_count_triangles_unpruned", "eh_count_4cliques_unpruned"):
+        for name in ("eh_count_triangles_unpruned", "eh_count_4cliques_unpruned", "eh_alg_bytes_k4"):
             getattr(L, name).argtypes = [vp]
+            getattr(L, name).restype = u64
+        for name in ("eh_count_triangles_range", "eh_count_4cliques_range"):
+            getattr(L, name).argtypes = [vp, u64, u64]
             getattr(L, name).restype = u64
         L.eh_symmetric_stats.argtypes = [vp, ctypes.POINTER(EHStats)]
         L.eh_symmetric_stats.restype = ctypes.c_int
@@ -87,6 +90,8 @@ def lib():
         L.eh_graph_export.restype = ctypes.c_int
         L.eh_free.argtypes = [vp]
         L.eh_free.restype = None
+        L.eh_release_cached_memory.argtypes = []
+        L.eh_release_cached_memory.restype = None
         L.eh_launch_count.argtypes = []
         L.eh_launch_count.restype = u64
         L.eh_last_status.argtypes = []
@@ -98,10 +103,11 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("eh_load_edges", "eh_load_edges_ex", "eh_count_triangles", "eh_count_4cliques",
+                    "eh_count_triangles_range", "eh_count_4cliques_range", "eh_alg_bytes_k4",
                     "eh_count_triangles_unpruned", "eh_count_4cliques_unpruned", "eh_symmetric_stats",
-                    "eh_triangles_per_vertex",
-                    "eh_count_lollipop", "eh_count_barbell", "eh_intersect", "eh_graph_stats", "eh_graph_export", "eh_free", "eh_launch_count", "eh_last_status",
-                    "eh_last_error")
+                    "eh_triangles_per_vertex", "eh_count_lollipop", "eh_count_barbell", "eh_intersect",
+                    "eh_graph_stats", "eh_graph_export", "eh_free", "eh_release_cached_memory", "eh_launch_count",
+                    "eh_last_status", "eh_last_error")
 
 
 def _raise():
@@ -189,6 +195,11 @@ class Graph:
         cfg.order = ORDERS[order]
         if stream is not None:
             cfg.stream = getattr(stream, "cuda_stream", stream)
+        elif sdev:
+            # device-resident inputs are ordered on the stream that produced them: torch's
+            # current stream (e.g. the copy .contiguous() may have just launched)
+            import torch
+            cfg.stream = torch.cuda.current_stream(self._ks.device).cuda_stream
         self._alloc = None
         if torch_allocator:
             import torch
@@ -231,6 +242,27 @@ class Graph:
             _raise()
         return int(r)
 
+    def count_triangles_range(self, r0: int, r1: int) -> int:
+        """Triangles whose earliest vertex has rank in [r0, r1) (eh_count_triangles_range)."""
+        r = lib().eh_count_triangles_range(self._h, int(r0), int(r1))
+        if r == EH_COUNT_ERROR:
+            _raise()
+        return int(r)
+
+    def count_4cliques_range(self, r0: int, r1: int) -> int:
+        """4-cliques whose earliest vertex has rank in [r0, r1) (eh_count_4cliques_range)."""
+        r = lib().eh_count_4cliques_range(self._h, int(r0), int(r1))
+        if r == EH_COUNT_ERROR:
+            _raise()
+        return int(r)
+
+    def alg_bytes_k4(self) -> int:
+        """B_K4(tau = 32) of SURVEY.md §8(d) (eh_alg_bytes_k4)."""
+        r = lib().eh_alg_bytes_k4(self._h)
+        if r == EH_COUNT_ERROR:
+            _raise()
+        return int(r)
+
     def count_triangles_unpruned(self) -> int:
         """NEXT-2: the triangle Generic-Join on the symmetric (unpruned) data = 6T (eh_count_triangles_unpruned)."""
         r = lib().eh_count_triangles_unpruned(self._h)
@@ -262,6 +294,13 @@ class Graph:
             t = np.zeros(max(n, 1), np.uint64)
             ptr = t.ctypes.data
         else:
+            import torch
+            if not (isinstance(out, torch.Tensor) and out.is_cuda):
+                raise TypeError("out must be a CUDA tensor (the host result is returned when out is None)")
+            if out.dtype not in (torch.int64, torch.uint64):
+                raise TypeError(f"out must be int64 or uint64, got {out.dtype}")
+            if not out.is_contiguous():
+                raise ValueError("out must be contiguous")
             if out.numel() < n:
                 raise ValueError(f"out has {out.numel()} elements, need {n}")
             t, ptr = out, out.data_ptr()
@@ -306,6 +345,11 @@ class Graph:
 def launch_count() -> int:
     """Kernels launched by libeh in this process (eh_launch_count)."""
     return int(lib().eh_launch_count())
+
+
+def release_cached_memory() -> None:
+    """Give the device memory libeh keeps idle back to the driver (eh_release_cached_memory)."""
+    lib().eh_release_cached_memory()
 
 
 def load_edges(src, dst, **kw) -> Graph:

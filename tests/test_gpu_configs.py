@@ -6,6 +6,13 @@ checks that the regenerated input has the recorded checksum, so a stored count
 always belongs to the exact edge list the GPU sees.  C2..C4 are additionally
 re-checked against a live oracle run in test_gpu_parity.py; C5 (1.34 B input
 edges; ~30 min of oracle time) is checked against the stored value only.
+
+4-cliques: every config whose golden holds `four_cliques` (C1-C4) is checked
+in full.  Where the full oracle 4-clique count is out of reach (C5), the GPU's
+rank-range counts are checked against the oracle's sampled rank windows
+(tests/golden/rank_ranges_oracle.json, tools/write_oracle_rank_goldens.py),
+on the full graph with the same kernels, and the full GPU count must equal
+the sum of its range counts over a partition of the ranks.
 """
 from __future__ import annotations
 
@@ -23,10 +30,19 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs_oracle.json")
 
 
+RANK_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "rank_ranges_oracle.json")
+
+
 def _gold():
     if not os.path.exists(GOLD):
         return {}
     return json.load(open(GOLD))["configs"]
+
+
+def _rank_gold():
+    if not os.path.exists(RANK_GOLD):
+        return {}
+    return json.load(open(RANK_GOLD))["configs"]
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
@@ -47,5 +63,16 @@ def test_config_vs_oracle_golden(name):
         assert (st.n_input, st.m_undirected, st.n_active, st.max_out_degree) == \
             (gold["n_input"], gold["m_undirected"], gold["n_active"], gold["max_out_degree"])
         assert g.count_triangles() == gold["triangles"]
+        k4 = g.count_4cliques()
         if "four_cliques" in gold:
-            assert g.count_4cliques() == gold["four_cliques"]
+            assert k4 == gold["four_cliques"]
+        rg = _rank_gold().get(name)
+        if rg is not None:
+            assert rg["checksum"] == gold["checksum"] and rg["n_active"] == st.n_active
+            for w in rg["windows"]:
+                assert g.count_triangles_range(w["r0"], w["r1"]) == w["triangles"], w
+                assert g.count_4cliques_range(w["r0"], w["r1"]) == w["four_cliques"], w
+        if "four_cliques" not in gold:
+            n = st.n_active
+            cut = n - 4096  # the top ranks hold most 4-cliques: two comparable halves of the work
+            assert g.count_4cliques_range(0, cut) + g.count_4cliques_range(cut, n) == k4

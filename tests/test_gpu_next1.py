@@ -151,9 +151,9 @@ def test_config_vs_oracle(name, golden_dir):
 
 @pytest.mark.parametrize("seed", range(2))
 def test_unstaged_cta_path(seed, monkeypatch):
-    # EH_PV_XCAP (test hook) lowers the CTA kernel's staging capacity, so every
+    # EH_TEST_PV_XCAP (test hook) lowers the CTA kernel's staging capacity, so every
     # |N+(x)| > 128 takes the unstaged path (global N+(x), global credit atomics).
-    monkeypatch.setenv("EH_PV_XCAP", "128")
+    monkeypatch.setenv("EH_TEST_PV_XCAP", "128")
     _check(*synth.rmat(14, 16, 777 + seed))
     a = 300
     _, t, lol, bar, tri = _gpu(*synth.complete_multipartite((a, a, a)))

@@ -89,7 +89,7 @@ def test_layout_and_binning_invariance(kw):
 
 @pytest.mark.parametrize("seed", range(2))
 def test_unstaged_cta_path(seed, monkeypatch):
-    monkeypatch.setenv("EH_TRI_XCAP", "128")
+    monkeypatch.setenv("EH_TEST_TRI_XCAP", "128")
     _check(*synth.rmat(12, 16, 8100 + seed))
 
 

@@ -129,9 +129,9 @@ def test_ids_near_u32_max_dictionary_path():
 
 @pytest.mark.parametrize("seed", range(2))
 def test_unstaged_cta_path(seed, monkeypatch):
-    # EH_TRI_XCAP (test hook) lowers the triangle CTA kernel's staging capacity:
+    # EH_TEST_TRI_XCAP (test hook) lowers the triangle CTA kernel's staging capacity:
     # every |N+(x)| > 128 then reads N+(x) from global memory (sorted-list mode).
-    monkeypatch.setenv("EH_TRI_XCAP", "128")
+    monkeypatch.setenv("EH_TEST_TRI_XCAP", "128")
     _check(*synth.rmat(14, 16, 555 + seed), k4=False)
     a = 300
     assert _gpu_counts(*synth.complete_multipartite((a, a, a)), k4=False)[0] == a**3
@@ -163,15 +163,15 @@ def test_constant_low_digits(stride):
 
 @pytest.mark.parametrize("xcap", [None, "128"])
 def test_wide_shape_tma_staging(monkeypatch, xcap):
-    # EH_TRI_WIDE (test hook) runs the wide (> 2^24 ids) triangle kernels on a small
+    # EH_TEST_TRI_WIDE (test hook) runs the wide (> 2^24 ids) triangle kernels on a small
     # graph: N+(x) staged by TMA (cp.async.bulk + mbarrier) double buffering; with
-    # EH_TRI_XCAP=128 the lists above 128 take the unstaged branch (mbarrier phase
+    # EH_TEST_TRI_XCAP=128 the lists above 128 take the unstaged branch (mbarrier phase
     # completed without a copy)
     src, dst = synth.rmat(14, 16, 41)
     ref = oracle.count_triangles(src, dst)
-    monkeypatch.setenv("EH_TRI_WIDE", "1")
+    monkeypatch.setenv("EH_TEST_TRI_WIDE", "1")
     if xcap:
-        monkeypatch.setenv("EH_TRI_XCAP", xcap)
+        monkeypatch.setenv("EH_TEST_TRI_XCAP", xcap)
     with eh.Graph(src, dst) as g:
         assert g.stats().max_out_degree > 128
         assert g.count_triangles() == ref
@@ -224,11 +224,11 @@ def test_layout_and_binning_invariance(kw):
 
 @pytest.mark.parametrize("seed", range(3))
 def test_hash_dedup_path(seed, monkeypatch):
-    """EH_DEDUP=hash: canonical keys deduplicated by a GPU hash set instead of
+    """EH_TEST_DEDUP=hash: canonical keys deduplicated by a GPU hash set instead of
     the one-sweep radix sort -- same trie, same counts."""
     src, dst = synth.rmat(13, 16, 70 + seed)
     base = _gpu_counts(src, dst)
-    monkeypatch.setenv("EH_DEDUP", "hash")
+    monkeypatch.setenv("EH_TEST_DEDUP", "hash")
     alt = _gpu_counts(src, dst)
     assert base[:2] == alt[:2] == (oracle.count_triangles(src, dst), oracle.count_4cliques(src, dst))
     assert base[2] == alt[2]
@@ -383,10 +383,10 @@ def test_block_layout_vs_oracle(seed):
 
 @pytest.mark.parametrize("kw", [dict(), dict(bin_small_max=2**32 - 1), dict(bin_large_min=1)])
 def test_block_layout_dense_and_hashed_x(kw, monkeypatch):
-    # K_400: every block dense; EH_TRI_XCAP forces hashed / sorted x structures (bit-by-bit dense path)
+    # K_400: every block dense; EH_TEST_TRI_XCAP forces hashed / sorted x structures (bit-by-bit dense path)
     from math import comb
     assert _gpu_counts(*synth.complete(400), k4=False, block_layout=True, **kw)[0] == comb(400, 3)
-    monkeypatch.setenv("EH_TRI_XCAP", "128")
+    monkeypatch.setenv("EH_TEST_TRI_XCAP", "128")
     assert _gpu_counts(*synth.complete(400), k4=False, block_layout=True, **kw)[0] == comb(400, 3)
     src, dst = synth.rmat(12, 16, 4)
     assert _gpu_counts(src, dst, k4=False, block_layout=True, **kw)[0] == oracle.count_triangles(src, dst)

@@ -21,10 +21,12 @@ NEXT1 = "--next1" in sys.argv
 NEXT2 = "--next2" in sys.argv
 NEXT3 = "--next3" in sys.argv
 NEXT4 = "--next4" in sys.argv
+K4ALL = "--k4" in sys.argv  # 4-clique count (and B_K4) on every config, not only C4
 names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"]
 reps = 5
 for name in names:
     cfg = synth.CONFIGS[name]
+    k4_reps = 1 if name == "C5" else reps  # C5's 4-clique count: one timed run
     src, dst = cfg.generate()
     n_in = src.size
     s = torch.from_numpy(src.view(np.int32)).cuda()
@@ -41,7 +43,7 @@ for name in names:
             e[1].record(st)
             t = g.count_triangles()
             e[2].record(st)
-            k = g.count_4cliques() if cfg.query == "4cliques" else None
+            k = g.count_4cliques() if (cfg.query == "4cliques" or K4ALL) and (r <= k4_reps) else None
             e[3].record(st)
             if NEXT1:  # t(v) into a device array, Lollipop, Barbell
                 e += [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -56,6 +58,8 @@ for name in names:
             st.synchronize()
             if r == 0:
                 stats = g.stats()
+                if k is not None and stats.n_active <= (1 << 24):
+                    b_k4 = g.alg_bytes_k4()
             g.close()
         if r == 0:
             res.update(triangles=t, four_cliques=k)
@@ -78,6 +82,9 @@ for name in names:
                step_edges_per_s=n_in / ((lt + tt) / 1e3), count_edges_per_s=n_in / (tt / 1e3))
     if k4s:
         res["k4_ms"] = statistics.median(k4s)
+        if stats.n_active <= (1 << 24):
+            res.update(alg_bytes_k4=b_k4, k4_gbs=b_k4 / res["k4_ms"] / 1e6,
+                       k4_roofline_frac=b_k4 / res["k4_ms"] / 1e6 / PEAK)
     if pvs:
         pv = statistics.median(pvs)
         pv_bytes = stats.alg_bytes_tri + 8 * stats.n_active  # B_tri reads + the t(v) array

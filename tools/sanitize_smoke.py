@@ -30,9 +30,9 @@ check(src, dst)                                   # warp + CTA kernels, sort ded
 check(src, dst, tau=2)                            # mostly uint rows (STREAM / SEARCH)
 check(src, dst, all_uint=True)
 check(src, dst, bin_small_max=1, bin_large_min=1)  # everything in the CTA kernels
-os.environ["EH_DEDUP"] = "hash"
+os.environ["EH_TEST_DEDUP"] = "hash"
 check(src, dst)
-del os.environ["EH_DEDUP"]
+del os.environ["EH_TEST_DEDUP"]
 ids = np.random.default_rng(1).choice(2**32 - 1, size=2**13, replace=False).astype(np.uint32)
 check(ids[src % ids.size], ids[dst % ids.size])   # dictionary path
 s, d = synth.complete(1100)                       # |N+(x)| > 1024: K4 fallback kernel
