@@ -4,9 +4,14 @@
 
 One STEP = one pass of the whole hot path over
 one synthetic input: eh_load_edges (canonicalise, radix sort, dedup, degree
-rank, orient, CSR, set layouts, work lists) + eh_count_triangles + eh_free.
-Workload: C3 = RMAT scale 22, edge factor 16, seed 3 (BASELINE.json
-configs[2], the configuration the ">= 40 % of HBM roofline" target names).
+rank, orient, CSR, set layouts, work lists) + eh_count_triangles (eh_free
+follows, outside the step's events).  Workload: C3 = RMAT scale 22, edge
+factor 16, seed 3 (BASELINE.json configs[2], the configuration the ">= 40 %
+of HBM roofline" target names).  `--query k4` (default config C4 =
+configs[3]) times the 4-clique step instead: eh_load_edges +
+eh_count_4cliques, roofline on B_K4 (eh_alg_bytes_k4).  The printed count is
+asserted equal to the oracle's stored value (tests/golden/configs_oracle.json)
+when one exists for the config.
 
   value  = input edges / device time of one step (inputs resident in HBM)
   e2e    = the same metric through the C ABI with HOST (pinned) inputs: the
@@ -15,9 +20,14 @@ configs[2], the configuration the ">= 40 % of HBM roofline" target names).
   roofline (dominant kernel = the triangle count): achieved = B_tri(tau=32)
            (computed exactly at load: eh_stats.alg_bytes_tri)
            / device time of eh_count_triangles; peak = MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline = the CPU oracle (oracle/, untuned) on a bounded sample of C3
+  cpu_baseline = the CPU oracle (oracle/, untuned) on this host, the paper's
+           protocol on the count loop (7 runs, drop the fastest
+           and slowest, mean; all host threads) plus its ingest timed once
+           (single-threaded qsort; reported separately, as the paper excludes
+           loading and index creation from query times)
 
-`--impl reference` times the oracle alone as the reference arm.
+`--impl reference` times the oracle alone as the reference arm: every step is
+one FULL count loop (all host threads) plus the once-timed ingest.
 Multi-GPU: the path does not shard (north star "one GPU"):
 `--gpus N` under torchrun runs N independent replicas ("replicas only",
 DESIGN.md); value = edges processed by all ranks / max-over-ranks time.
@@ -42,13 +52,26 @@ import synth  # noqa: E402  (input generator; no method arithmetic)
 
 
 METRIC = "triangles counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)"
+METRIC_K4 = "4-cliques counted: input edges/sec and achieved HBM GB/s vs peak (1 B200)"
+GOLD = os.path.join(ROOT, "tests", "golden", "configs_oracle.json")
 
 
-def _workload(cfg) -> str:
+def _workload(cfg, query="tri") -> str:
+    q = "4-clique count" if query == "k4" else "triangle count"
     if cfg.kind == "er":
-        return f"{cfg.name}: ER G(n={cfg.n}, p={cfg.p}), seed {cfg.seed}; triangle count"
+        return f"{cfg.name}: ER G(n={cfg.n}, p={cfg.p}), seed {cfg.seed}; {q}"
     return (f"{cfg.name}: RMAT scale {cfg.scale}, edge factor {cfg.edge_factor}, (a,b,c)=(.57,.19,.19), "
-            f"seed {cfg.seed}; triangle count")
+            f"seed {cfg.seed}; {q}")
+
+
+def _golden(cfg, src, dst, query):
+    """The oracle's stored count for this exact input (checksum-matched), else None."""
+    if not os.path.exists(GOLD):
+        return None
+    g = json.load(open(GOLD))["configs"].get(cfg.name)
+    if not g or g.get("checksum") != str(synth.checksum(src, dst)):
+        return None
+    return g.get("four_cliques" if query == "k4" else "triangles")
 
 
 def _peaks():
@@ -159,26 +182,39 @@ def _flush_l2(buf):
 
 
 # ------------------------------------------------------------------ CPU oracle --
-def _oracle_sample(src, dst, frac_slices: int = 16, slices: int = 1):
-    """Oracle ingest on the full input, then the triangle loop over `slices` of
-    `frac_slices` equal slices of the outer x loop; returns (t_ingest, t_count_est,
-    threads, description)."""
+def _oracle_protocol(src, dst, query: str, runs: int):
+    """The CPU oracle on this host: ingest timed once (it is single-threaded), then
+    the full count loop `runs` times with all host threads; the paper's protocol
+     keeps the mean of the runs without the fastest and slowest.
+    Returns (t_ingest_s, count_mean_s, per-run seconds, threads, count)."""
     import oracle
     threads = oracle.default_threads()
     t0 = time.perf_counter()
     g = oracle.Graph(src, dst)
     t_ing = time.perf_counter() - t0
-    nv = g.n_vertices
-    t0 = time.perf_counter()
-    for k in range(slices):
-        g.count_triangles_range(nv * k // frac_slices, nv * (k + 1) // frac_slices, threads)
-    t_cnt = (time.perf_counter() - t0) * frac_slices / slices
+    times, counts = [], set()
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        counts.add(g.count_4cliques(threads) if query == "k4" else g.count_triangles(threads))
+        times.append(time.perf_counter() - t0)
     g.close()
-    return g, t_ing, t_cnt, threads
+    kept = sorted(times)[1:-1] if len(times) >= 3 else times
+    return t_ing, statistics.mean(kept), times, threads, counts.pop() if len(counts) == 1 else sorted(counts)
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, cfg, src, dst, n_in):
-    """Reference arm: the CPU oracle as it stands on this host's cores."""
+    """Reference arm: the CPU oracle as it stands on this host's cores.  Every step
+    is one full count loop; the oracle ingest is timed once and added to each step."""
     import oracle
     dist, rank, ws, _ = _dist()
     if rank != 0:
@@ -187,29 +223,28 @@ def run_reference(args, cfg, src, dst, n_in):
     t0 = time.perf_counter()
     g = oracle.Graph(src, dst)
     t_ing = time.perf_counter() - t0
-    nv = g.n_vertices
-    S = 64  # each step: 1/64 of the outer x loop + 1/64 of the (once-measured) ingest time
-    times = []
+    times, counts = [], set()
     for i in range(args.warmup + args.steps):
-        k = i % S
         t0 = time.perf_counter()
-        g.count_triangles_range(nv * k // S, nv * (k + 1) // S, threads)
-        dt = time.perf_counter() - t0 + t_ing / S
+        counts.add(g.count_4cliques(threads) if args.query == "k4" else g.count_triangles(threads))
+        dt = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append(dt)
+            times.append(dt + t_ing)
     g.close()
-    step_full = statistics.mean(times) * S  # estimated full-workload time
-    value = n_in / step_full
-    sample = (f"oracle ingest of the full {cfg.name} input timed once ({t_ing:.2f} s); each step = one 1/{S} "
-              f"slice of the outer x loop of the triangle nest + 1/{S} of the ingest time; value = n_in / "
-              f"(64 x mean step)")
-    line = {"impl": "reference", "metric": METRIC, "value": value,
+    step = statistics.mean(times)
+    value = n_in / step
+    sample = (f"full {cfg.name} {'4-clique' if args.query == 'k4' else 'triangle'} count loop every step "
+              f"({threads} threads, mean {statistics.mean(times) - t_ing:.2f} s) + the oracle ingest of the full "
+              f"input timed once ({t_ing:.2f} s, single-threaded) added to each step; host: {_cpu_model()}")
+    line = {"impl": "reference", "metric": METRIC_K4 if args.query == "k4" else METRIC, "value": value,
             "unit": "input edges/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": _workload(cfg), "n_input": n_in},
+            "config": {"workload": _workload(cfg, args.query), "n_input": n_in},
+            "count": counts.pop() if len(counts) == 1 else sorted(counts),
             "cpu_baseline": {"value": value, "unit": "input edges/s", "cores": threads, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "ingest_s": t_ing, "ingest_threads": 1,
+                             "count_s": [t - t_ing for t in times]},
             "e2e": {"value": value, "unit": "input edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -220,6 +255,7 @@ def run_gpu(args, cfg, src, dst, n_in):
     import paper_1503_02368_b200 as eh
 
     dist, rank, ws, local = _dist()
+    k4 = args.query == "k4"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
@@ -244,10 +280,14 @@ def run_gpu(args, cfg, src, dst, n_in):
             else:
                 g = eh.Graph(d_src, d_dst, stream=stream)
             ev[1].record(stream)
-            c = g.count_triangles()
+            c = g.count_4cliques() if k4 else g.count_triangles()
             ev[2].record(stream)
             stream.synchronize()
-            st = g.stats() if want_stats else None
+            st = None
+            if want_stats:
+                st = g.stats()
+                if k4:
+                    st.alg_bytes_k4 = g.alg_bytes_k4()
             g.close()
         stream.synchronize()
         return ev[0].elapsed_time(ev[2]), ev[1].elapsed_time(ev[2]), c, st
@@ -288,8 +328,11 @@ def run_gpu(args, cfg, src, dst, n_in):
         e2e_ms.append(t)
         counts.add(c)
     if len(counts) != 1:
-        raise RuntimeError(f"non-deterministic triangle counts: {counts}")
+        raise RuntimeError(f"non-deterministic counts: {counts}")
     T = counts.pop()
+    gold = _golden(cfg, src, dst, args.query)
+    if gold is not None and T != gold:
+        raise RuntimeError(f"count {T} differs from the oracle's stored value {gold}")
     mean_step = statistics.mean(step_ms)
     mean_count = statistics.mean(count_ms)
     mean_e2e = statistics.mean(e2e_ms)
@@ -297,35 +340,46 @@ def run_gpu(args, cfg, src, dst, n_in):
     e2e_value, mean_e2e_max = aggregate(dist, ws, n_in, mean_e2e, dev)
     if rank != 0:
         return
-    achieved = st.alg_bytes_tri / (mean_count / 1e3) / 1e9
+    alg = st.alg_bytes_k4 if k4 else st.alg_bytes_tri
+    achieved = alg / (mean_count / 1e3) / 1e9
     line = {
-        "metric": METRIC,
+        "metric": METRIC_K4 if k4 else METRIC,
         "value": value, "unit": "input edges/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean_step_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": _workload(cfg),
+        "config": {"workload": _workload(cfg, args.query),
                    "n_input": n_in, "m_undirected": st.m_undirected, "n_active": st.n_active,
                    "parallelism": "replicas only" if ws > 1 else "1 GPU",
-                   "l2": "512 MiB flush write between timed steps (outside the per-step events); inputs 537 MB > L2",
-                   "step": "eh_load_edges(device inputs) + eh_count_triangles + eh_free"},
-        "triangles": T,
+                   "l2": "512 MiB flush write between timed steps (outside the per-step events); inputs "
+                         f"{8 * n_in / 1e6:.0f} MB",
+                   "step": ("eh_load_edges(device inputs) + " + ("eh_count_4cliques" if k4 else "eh_count_triangles")
+                            + " (eh_free after the step's events)")},
+        ("four_cliques" if k4 else "triangles"): T,
+        "oracle_golden_match": gold is not None,
         "count_ms": mean_count, "load_ms": mean_step - mean_count,
         "count_edges_per_s": n_in / (mean_count / 1e3),
-        "triangles_per_s": T / (mean_count / 1e3),
+        ("four_cliques_per_s" if k4 else "triangles_per_s"): T / (mean_count / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _traffic(), "peak_kind": peak_kind, "kernel": "k_tri_*  (eh_count_triangles)",
-                     "alg_bytes_per_launch": st.alg_bytes_tri},
+                     "traffic": None if k4 else _traffic(), "peak_kind": peak_kind,
+                     "kernel": "k_k4_* (eh_count_4cliques)" if k4 else "k_tri_* (eh_count_triangles)",
+                     "alg_bytes": "B_K4(tau=32)" if k4 else "B_tri(tau=32)", "alg_bytes_per_launch": alg},
         "e2e": {"value": e2e_value, "unit": "input edges/s",
                 "h2d_bytes_per_step": 8 * n_in, "d2h_bytes_per_step": 8},
         "gpu_launches": launches,
         "clocks": clk,
     }
     if not args.no_cpu_baseline and ws == 1:
-        og, t_ing, t_cnt, threads = _oracle_sample(src, dst, frac_slices=16, slices=1)
-        line["cpu_baseline"] = {"value": n_in / (t_ing + t_cnt), "unit": "input edges/s", "cores": threads,
-                                "kind": "oracle",
-                                "sample": f"oracle ingest of the full {cfg.name} input ({t_ing:.1f} s) + the triangle "
-                                          f"loop over 1/16 of the outer x loop, scaled x16 ({t_cnt:.1f} s est.)"}
+        runs = args.cpu_runs or (3 if k4 else 7)
+        t_ing, t_cnt, per_run, threads, oc = _oracle_protocol(src, dst, args.query, runs)
+        if oc != T:
+            raise RuntimeError(f"GPU count {T} differs from the oracle's {oc}")
+        line["cpu_baseline"] = {
+            "value": n_in / (t_ing + t_cnt), "unit": "input edges/s", "cores": threads, "kind": "oracle",
+            "sample": (f"full {cfg.name} input: oracle ingest timed once ({t_ing:.1f} s, single-threaded qsort) + "
+                       f"the full {'4-clique' if k4 else 'triangle'} count loop, {runs} runs on {threads} threads, "
+                       f"mean without the fastest and slowest ({t_cnt:.2f} s; PAPER.md:756); host: {_cpu_model()}"),
+            "ingest_s": t_ing, "ingest_threads": 1, "count_s": t_cnt, "count_runs_s": per_run,
+            "count_value": n_in / t_cnt}
     print(json.dumps(line), flush=True)
 
 
@@ -335,9 +389,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="eh", choices=["eh", "reference"])
-    ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(synth.CONFIGS),
+                    help="default C3 (triangles) or C4 (--query k4)")
+    ap.add_argument("--query", default="tri", choices=["tri", "k4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-runs", type=int, default=0, help="oracle count-loop runs (default 7; 3 for k4)")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "C4" if args.query == "k4" else "C3"
     if args.warmup < 3 and args.impl == "eh":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     cfg = synth.CONFIGS[args.config]

@@ -510,7 +510,7 @@ uint64_t k4_impl(eh_graph* g) {
       const uint64_t nbig = select_if(nlarge, BigPred{g->desc, wl}, BigEmit{g->desc, wl, bx.p, brows.p}, g->alloc, s);
       DBuf<uint64_t> boff(g->alloc, nbig + 1), tot(g->alloc, 1);
       scan_exclusive_u32(brows.p, boff.p, nbig, tot.p, g->alloc, s);
-      const uint64_t nrows = read_scalar(tot.p, s);
+      const uint64_t nrows = nbig ? read_scalar(tot.p, s) : 0;
       // P's bitmap over all ids on chip when it fits next to the P list (C2: 32 KB, C4: 80 KB)
       const uint32_t bm_words = (g->n_act + 127) / 128 * 4 <= kBigBmMaxWords ? (uint32_t)((g->n_act + 127) / 128 * 4) : 0u;
       const size_t smem = ((size_t)kBigPCap + bm_words) * 4;
@@ -519,10 +519,12 @@ uint64_t k4_impl(eh_graph* g) {
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_k4_big<kU>, kBigThreads, smem));
       const unsigned gb = (unsigned)std::min<uint64_t>(nrows, (uint64_t)kSMs * std::max(1, per_sm));
       const uint32_t stride = (uint32_t)g->max_dplus;  // |P| <= max |N+(x)|
-      DBuf<uint32_t> scratch(g->alloc, (size_t)gb * stride);
-      k_k4_big<kU><<<gb, kBigThreads, smem, s>>>(g->desc, g->col, g->bs, bx.p, boff.p, nbig, nrows, scratch.p,
-                                                  stride, g->d_counter, bm_words);
-      EH_LAUNCH("k_k4_big");
+      DBuf<uint32_t> scratch(g->alloc, (size_t)std::max(1u, gb) * stride);
+      if (nrows) {  // a rank range (eh_count_4cliques_range) may hold none of the big x
+        k_k4_big<kU><<<gb, kBigThreads, smem, s>>>(g->desc, g->col, g->bs, bx.p, boff.p, nbig, nrows, scratch.p,
+                                                    stride, g->d_counter, bm_words);
+        EH_LAUNCH("k_k4_big");
+      }
       EH_CUDA(cudaStreamSynchronize(s));  // scratch is released on return
     }
   }
