@@ -90,6 +90,11 @@ typedef struct {
    * (PAPER.md:1065-1153); counts never depend on it.  EH_ORDER_* below;
    * 0 = EH_ORDER_DEGREE, the paper's default. */
   uint32_t order;
+  /* a7 thread class: the x with 2 <= |N+(x)| <= bin_thread_max (within class 0) run
+   * one THREAD per x in the triangle count (their <= C(d, 2) probes are too few to
+   * occupy a warp).  0 -> 8; 1 disables the class; clamped to
+   * bin_small_max and to 16.  Counts do not depend on it. */
+  uint32_t bin_thread_max;
 } eh_config;
 
 /* Node orderings (readings in DESIGN.md c20).  Each names the

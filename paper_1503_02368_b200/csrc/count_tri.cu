@@ -443,6 +443,76 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
+// ----------------------------------------------------------- thread kernel --
+// a7 thread class: one THREAD per x with 2 <= |N+(x)| <= bin_thread_max (C3:
+// 923 k of the 1.56 M warp-class x, but only 2.7 M of their 15 M rows and 7 M
+// of their 161 M wedges).  A warp per such x spends its time on the per-x
+// staging / classification / ordering with most lanes idle; here 32 x run side
+// by side.  Row (x, y = x_i): every a in A = N+(x) after y is a bit probe of
+// y's bitset (uint cap bitset) or, y uint, a binary search of N+(y) that
+// resumes where the previous a stopped (A is increasing; the galloping side
+// of the uint hybrid) -- |A| <= 15, so the min property always
+// favours probing A over streaming N+(y).  N+(x) is staged per thread in
+// shared memory with an odd stride (a warp's 32 threads hit 32 banks).
+constexpr int kTMax = 16;
+constexpr int kTBlock = 256;
+constexpr int kTStride = kTMax + 1;
+
+__global__ void __launch_bounds__(kTBlock) k_tri_thread(const uint4* __restrict__ desc,
+                                                        const uint32_t* __restrict__ col,
+                                                        const uint32_t* __restrict__ bs,
+                                                        const uint32_t* __restrict__ work, uint64_t nwork,
+                                                        unsigned long long* __restrict__ ctr) {
+  __shared__ uint32_t sxs[kTBlock * kTStride];
+  uint32_t* xs = sxs + threadIdx.x * kTStride;
+  unsigned long long cnt = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nwork; k += stride) {
+    const uint32_t x = __ldg(work + k);
+    const uint4 dx = __ldg(desc + x);
+    const uint32_t d = dx.y;  // 2 <= d <= kTMax
+    const uint4* xg = reinterpret_cast<const uint4*>(col) + dx.x;
+    for (uint32_t q = 0; q < (d + 3) / 4; ++q) {
+      const uint4 v = __ldg(xg + q);
+      xs[4 * q] = v.x;
+      xs[4 * q + 1] = v.y;
+      xs[4 * q + 2] = v.z;
+      xs[4 * q + 3] = v.w;
+    }
+    for (uint32_t i = 0; i + 1 < d; ++i) {
+      const YInfo y = yinfo(desc, xs[i]);
+      if (y.len == 0) continue;
+      if (y.c1 > y.c0) {
+        for (uint32_t j = i + 1; j < d; ++j) cnt += probe_bits(bs, y, xs[j]);
+      } else {
+        const uint32_t* L = col + (uint64_t)y.list * 4;
+        uint32_t lo = 0;
+        for (uint32_t j = i + 1; j < d; ++j) {
+          const uint32_t e = xs[j];
+          uint32_t len = y.len - lo;
+          while (len > 0) {
+            const uint32_t h = len >> 1;
+            if (__ldg(L + lo + h) < e) { lo += h + 1; len -= h + 1; } else { len = h; }
+          }
+          if (lo == y.len) break;
+          cnt += (__ldg(L + lo) == e);
+        }
+      }
+    }
+  }
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr[0], cnt);
+}
+
+void launch_thread(eh_graph* g, uint64_t nt) {
+  if (nt == 0) return;
+  int per_sm = 0;
+  EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_thread, kTBlock, 0));
+  const unsigned grid = (unsigned)std::min<uint64_t>((nt + kTBlock - 1) / kTBlock, (uint64_t)kSMs * std::max(1, per_sm));
+  k_tri_thread<<<grid, kTBlock, 0, g->stream>>>(g->desc, g->col, g->bs, g->work, nt, g->d_counter);
+  EH_LAUNCH("k_tri_thread");
+}
+
 // ---------------------------------------------- bulk async copy (TMA) --
 // 1-D cp.async.bulk global -> shared, completion tracked by an mbarrier
 // (transaction bytes); one thread arms and issues, every thread waits.
@@ -776,7 +846,10 @@ uint64_t count_impl(eh_graph* g) {
     else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4, 16>(g, nsmall, nlarge, xcap);
     else launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, xcap);
   }
-  if (nsmall) {
+  // a7 thread class (the head of class 0; pruned set-level nest only)
+  const uint64_t nt = (!kUnpruned && !kBlock) ? g->n_thread : 0;
+  launch_thread(g, nt);
+  if (nsmall > nt) {
     // staging sized for class 0 (|N+(x)| <= 64 by default): 30 KB instead of 43 KB
     // per 8-warp CTA, one more CTA per SM (measured: C3 9.48 -> 9.41 ms)
     // SEARCH rows start inside one of 8 pivot slices on the larger graphs (> 2^20 active
@@ -784,14 +857,16 @@ uint64_t count_impl(eh_graph* g) {
     const bool big = g->n_act > (1ull << 20);
     // min 6 CTAs per SM: 40 registers (a few spilled bytes) for one more resident CTA
     // (measured C3 8.59 -> 8.38 ms, C4 1.458 -> 1.419, C2 0.316 -> 0.313)
-    if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16, true>(g, nsmall);
-    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, nsmall);
-    else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, nsmall);
-    else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, nsmall);
+    const uint32_t* w0 = g->work + nt;
+    const uint64_t n0 = nsmall - nt;
+    if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16, true>(g, n0, w0);
+    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, n0, w0);
+    else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, n0, w0);
+    else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, n0, w0);
     else if (!kUnpruned && !kBlock && g->class0_max <= 64) {  // wide: class 0 with 64-entry staging, min 6 CTAs/SM
-      launch_warp<kUnpruned, kBlock, 64, 6, kG, 64, true>(g, g->n_work[0], g->work, 1u);
+      launch_warp<kUnpruned, kBlock, 64, 6, kG, 64, true>(g, g->n_work[0] - nt, w0, 1u);
       launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall - g->n_work[0], g->work + g->n_work[0], 6u);
-    } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall);
+    } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, n0, w0);
   }
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
@@ -808,5 +883,6 @@ uint64_t count_triangles(eh_graph* g) {
 uint64_t count_triangles_unpruned(eh_graph* g) { return count_impl<true, false>(symmetric_trie(g)); }
 
 uint32_t tri_warp_max_degree() { return kWarpMaxD; }
+uint32_t tri_thread_max_degree() { return kTMax; }
 
 }  // namespace eh

@@ -96,6 +96,7 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       g->min_bitset_card = c.min_bitset_card ? c.min_bitset_card : 2;
       g->bin_small_max = c.bin_small_max;
       g->bin_large_min = c.bin_large_min;
+      g->bin_thread_max = c.bin_thread_max;
       if (c.order > EH_ORDER_SHINGLE) eh::fail(EH_EINVAL, "eh_load_edges: unknown order %u", c.order);
       g->order = c.order;
       if (c.stream) {

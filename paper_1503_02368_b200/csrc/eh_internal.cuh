@@ -205,7 +205,7 @@ struct eh_graph {
   bool own_stream = false;
   eh::Allocator alloc;
   uint32_t flags = 0, tau = 32, min_bitset_card = 2;
-  uint32_t bin_small_max = 0, bin_large_min = 0;
+  uint32_t bin_small_max = 0, bin_large_min = 0, bin_thread_max = 0;
   uint32_t order = 0;  // NEXT-4: EH_ORDER_*
 
   uint64_t n_input = 0, m = 0, n_act = 0, max_dplus = 0;
@@ -235,6 +235,7 @@ struct eh_graph {
   uint32_t* work = nullptr;
   uint32_t* work_lpt = nullptr;  // same lists, classes 1-2 heaviest first (work_lpt(), on demand)
   uint64_t n_work[3] = {0, 0, 0};
+  uint64_t n_thread = 0;    // the first n_thread entries of class 0: the thread class (d <= bin_thread_max)
   uint32_t class0_max = 0;  // largest |N+(x)| of class 0 (the warp kernels' staging bound)
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
@@ -274,12 +275,14 @@ class WorkRange {
   eh_graph* g_;
   uint32_t* saved_work_;
   uint32_t* saved_lpt_;
-  uint64_t saved_n_[3];
+  uint64_t saved_n_[3], saved_nt_;
   DBuf<uint32_t> work_, lpt_;
 };
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);
 uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept
+uint32_t tri_thread_max_degree();  // largest |N+(x)| the thread-per-x kernel accepts
+constexpr uint32_t kThreadMaxDefault = 8;  // default bin_thread_max (a7 thread class)
 uint64_t count_4cliques(eh_graph* g);
 // count_pv.cu (NEXT-1): t(v) per rank into a device array; Lollipop / Barbell 128-bit counts
 void triangles_per_vertex(eh_graph* g, unsigned long long* d_t);

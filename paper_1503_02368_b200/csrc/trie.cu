@@ -95,13 +95,14 @@ __global__ void k_stats(const uint4* __restrict__ desc, const uint32_t* __restri
   }
 }
 
-// Work lists: vertices with |N+(x)| >= 2 (others close no triangle) by class.
-struct WorkClass {  // 0: 2 <= d < h0, 1: h0 <= d < h1, 2: d >= h1 (and d >= 2); -1: d < 2
+// Work lists: vertices with |N+(x)| >= 2 (others close no triangle) by class;
+// the thread class (2 <= d < ht) is emitted first, as the head of class 0.
+struct WorkClass {  // 0: 2 <= d < ht, 1: ht <= d < h0, 2: h0 <= d < h1, 3: d >= h1 (and d >= 2); -1: d < 2
   const uint4* desc;
-  uint32_t h0, h1;
+  uint32_t ht, h0, h1;
   __device__ int operator()(uint64_t v) const {
     const uint32_t d = desc[v].y;
-    return d < 2 ? -1 : d < h0 ? 0 : d < h1 ? 1 : 2;
+    return d < 2 ? -1 : d < ht ? 0 : d < h0 ? 1 : d < h1 ? 2 : 3;
   }
 };
 struct WorkEmit3 {
@@ -128,12 +129,12 @@ __global__ void k_work_unkey(const uint64_t* __restrict__ key, uint64_t n, uint3
 // class-major list keeps its class iff the vertex lies in [r0, r1).
 struct RangeClass {
   const uint32_t* w;
-  uint64_t e0, e1;  // class boundaries (positions)
+  uint64_t et, e0, e1;  // class boundaries (positions): thread head of class 0, classes 0, 1
   uint32_t r0, r1;
   __device__ int operator()(uint64_t k) const {
     const uint32_t v = w[k];
     if (v < r0 || v >= r1) return -1;
-    return k < e0 ? 0 : k < e1 ? 1 : 2;
+    return k < et ? 0 : k < e0 ? 1 : k < e1 ? 2 : 3;
   }
 };
 struct RangeEmit {
@@ -178,6 +179,7 @@ __global__ void k_k4_bytes(const uint4* __restrict__ desc, const uint32_t* __res
 WorkRange::WorkRange(eh_graph* g, uint64_t r0, uint64_t r1) : g_(g) {
   saved_work_ = g->work;
   saved_lpt_ = g->work_lpt;
+  saved_nt_ = g->n_thread;
   for (int c = 0; c < 3; ++c) saved_n_[c] = g->n_work[c];
   const uint64_t n = saved_n_[0] + saved_n_[1] + saved_n_[2];
   r1 = std::min<uint64_t>(r1, g->n_act);
@@ -185,17 +187,20 @@ WorkRange::WorkRange(eh_graph* g, uint64_t r0, uint64_t r1) : g_(g) {
   // the LPT list is filtered too, so the kernels that take it keep their order
   const uint32_t* lpt = (n && g->work_lpt) ? g->work_lpt : nullptr;
   work_ = DBuf<uint32_t>(g->alloc, std::max<uint64_t>(1, n));
-  uint64_t starts[4] = {0, 0, 0, 0};
-  partition_k<3>(n, RangeClass{saved_work_, saved_n_[0], saved_n_[0] + saved_n_[1], (uint32_t)r0, (uint32_t)r1},
-                 RangeEmit{saved_work_, work_.p}, starts, g->alloc, g->stream);
-  if (lpt) {
+  uint64_t starts[5] = {0, 0, 0, 0, 0};
+  const RangeClass rc{saved_work_, saved_nt_, saved_n_[0], saved_n_[0] + saved_n_[1], (uint32_t)r0, (uint32_t)r1};
+  partition_k<4>(n, rc, RangeEmit{saved_work_, work_.p}, starts, g->alloc, g->stream);
+  if (lpt) {  // same class boundaries (the LPT order permutes inside classes 1-2 only)
     lpt_ = DBuf<uint32_t>(g->alloc, std::max<uint64_t>(1, n));
-    partition_k<3>(n, RangeClass{lpt, saved_n_[0], saved_n_[0] + saved_n_[1], (uint32_t)r0, (uint32_t)r1},
-                   RangeEmit{lpt, lpt_.p}, starts, g->alloc, g->stream);
+    RangeClass rl = rc;
+    rl.w = lpt;
+    uint64_t st2[5];
+    partition_k<4>(n, rl, RangeEmit{lpt, lpt_.p}, st2, g->alloc, g->stream);
   }
   g->work = work_.p;
   g->work_lpt = lpt ? lpt_.p : nullptr;
-  for (int c = 0; c < 3; ++c) g->n_work[c] = starts[c + 1] - starts[c];
+  g->n_thread = starts[1] - starts[0];
+  for (int c = 0; c < 3; ++c) g->n_work[c] = starts[c + 2] - starts[c == 0 ? 0 : c + 1];
 }
 
 WorkRange::~WorkRange() {
@@ -204,6 +209,7 @@ WorkRange::~WorkRange() {
   // the range: it is dropped here (its memory stays with the handle until eh_free)
   g_->work = saved_work_;
   g_->work_lpt = saved_lpt_;
+  g_->n_thread = saved_nt_;
   for (int c = 0; c < 3; ++c) g_->n_work[c] = saved_n_[c];
 }
 
@@ -384,11 +390,17 @@ void build_worklists(eh_graph* g) {
   hi[1] = std::max<uint64_t>(lo[1], large_min);
   lo[2] = hi[1];
   hi[2] = 1ull << 33;
-  // one stable 3-way partition (class-major, each class in rank order)
-  uint64_t starts[4];
-  partition_k<3>(n, WorkClass{g->desc, (uint32_t)hi[0], (uint32_t)std::min<uint64_t>(hi[1], 0xFFFFFFFFull)},
+  // thread class = the head of class 0 with d <= thread_max (a7)
+  const uint64_t tmax = std::min<uint64_t>(g->bin_thread_max ? g->bin_thread_max : kThreadMaxDefault,
+                                           std::min<uint64_t>(hi[0] - 1, tri_thread_max_degree()));
+  const uint64_t ht = std::max<uint64_t>(2, tmax + 1);
+  // one stable 4-way partition (class-major, each class in rank order)
+  uint64_t starts[5];
+  partition_k<4>(n, WorkClass{g->desc, (uint32_t)ht, (uint32_t)hi[0], (uint32_t)std::min<uint64_t>(hi[1], 0xFFFFFFFFull)},
                  WorkEmit3{g->work}, starts, al, s);
-  for (int c = 0; c < 3; ++c) g->n_work[c] = starts[c + 1] - starts[c];
+  g->n_thread = starts[1] - starts[0];
+  g->n_work[0] = starts[2] - starts[0];
+  for (int c = 1; c < 3; ++c) g->n_work[c] = starts[c + 2] - starts[c + 1];
 }
 
 // The work lists with classes 1 and 2 each in descending-d order (heaviest x

@@ -32,7 +32,8 @@ class EHConfig(ctypes.Structure):
     _fields_ = [("bitset_tau", ctypes.c_uint32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("dev_alloc", _ALLOC_FN), ("dev_free", _FREE_FN), ("alloc_ctx", ctypes.c_void_p),
                 ("flags", ctypes.c_uint32), ("bin_small_max", ctypes.c_uint32), ("bin_large_min", ctypes.c_uint32),
-                ("min_bitset_card", ctypes.c_uint32), ("order", ctypes.c_uint32)]
+                ("min_bitset_card", ctypes.c_uint32), ("order", ctypes.c_uint32),
+                ("bin_thread_max", ctypes.c_uint32)]
 
 ORDERS = {"degree": 0, "rev_degree": 1, "random": 2, "bfs": 3, "hybrid": 4, "shingle": 5}
 
@@ -172,7 +173,8 @@ class Graph:
 
     def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False,
                  block_layout: bool = False, order: str = "degree", bin_small_max: int = 0,
-                 bin_large_min: int = 0, min_bitset_card: int = 0, stream=None, device: int | None = None,
+                 bin_large_min: int = 0, bin_thread_max: int = 0, min_bitset_card: int = 0, stream=None,
+                 device: int | None = None,
                  torch_allocator: bool = False):
         L = lib()
         n = _numel(src)
@@ -191,6 +193,7 @@ class Graph:
             cfg.device = device
         cfg.bin_small_max = bin_small_max
         cfg.bin_large_min = bin_large_min
+        cfg.bin_thread_max = bin_thread_max
         cfg.min_bitset_card = min_bitset_card
         cfg.order = ORDERS[order]
         if stream is not None:

@@ -215,7 +215,8 @@ def test_block_cache_reuse_across_streams():
                                 dict(block_layout=True, tau=2), dict(block_layout=True, bin_large_min=1),
                                 dict(min_bitset_card=1), dict(bin_small_max=2**32 - 1),
                                 dict(bin_small_max=1, bin_large_min=1), dict(bin_small_max=1, bin_large_min=2**32 - 1),
-                                dict(torch_allocator=True)])
+                                dict(torch_allocator=True), dict(bin_thread_max=1), dict(bin_thread_max=2),
+                                dict(bin_thread_max=16), dict(bin_thread_max=16, bin_small_max=4)])
 def test_layout_and_binning_invariance(kw):
     src, dst = synth.rmat(13, 16, 5)
     base = _gpu_counts(src, dst)[:2]

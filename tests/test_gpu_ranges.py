@@ -66,7 +66,7 @@ def test_ranges_kn_closed_form_and_edges():
 
 
 @pytest.mark.parametrize("kw", [dict(bin_small_max=2**32 - 1), dict(bin_large_min=1), dict(block_layout=True),
-                                dict(all_uint=True)])
+                                dict(all_uint=True), dict(bin_thread_max=1), dict(bin_thread_max=16)])
 def test_ranges_invariant_under_classes_and_layouts(kw):
     src, dst = synth.rmat(13, 16, 4100)
     og = oracle.Graph(src, dst)
