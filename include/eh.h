@@ -92,7 +92,7 @@ typedef struct {
   uint32_t order;
   /* a7 thread class: the x with 2 <= |N+(x)| <= bin_thread_max (within class 0) run
    * one THREAD per x in the triangle count (their <= C(d, 2) probes are too few to
-   * occupy a warp).  0 -> 8; 1 disables the class; clamped to
+   * occupy a warp).  0 -> 8 (4 above 2^24 active ids); 1 disables the class; clamped to
    * bin_small_max and to 16.  Counts do not depend on it. */
   uint32_t bin_thread_max;
 } eh_config;
@@ -141,6 +141,27 @@ typedef struct {
  */
 eh_graph* eh_load_edges(const uint32_t* src, const uint32_t* dst, uint64_t n);
 eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg);
+
+/*
+ * eh_count_batch -- the whole path (eh_load_edges + the COUNT(*) of `query` +
+ * eh_free) for k independent edge lists, with the upload of list i+1 (a copy
+ * engine, on a separate stream) overlapping the trie build and count of list i
+ * on the SMs.  Same semantics per list as eh_load_edges_ex (with cfg) followed
+ * by eh_count_triangles / eh_count_4cliques.
+ *  src[i], dst[i], n[i] : list i in HOST memory (page-locked memory is needed for
+ *                         the overlap; pageable memory works, serialised)
+ *  query                : EH_QUERY_TRIANGLES or EH_QUERY_4CLIQUES
+ *  cfg                  : may be NULL; EH_INPUT_ON_DEVICE is rejected; cfg->stream
+ *                         (else a library-owned blocking stream) runs the compute
+ *  counts[k]            : caller-owned host array, receives the k counts
+ * Two device input buffers of 8 max(n) bytes are held for the call.  Returns
+ * EH_OK, EH_EINVAL, EH_ENOMEM or EH_ECUDA (counts of lists before a failure are
+ * written).
+ */
+#define EH_QUERY_TRIANGLES 0u
+#define EH_QUERY_4CLIQUES 1u
+int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const uint64_t* n, uint64_t k,
+                   uint32_t query, const eh_config* cfg, uint64_t* counts);
 
 /*
  * eh_count_triangles -- COUNT(*) of Triangle(x,y,z) on the pruned relation:

@@ -64,12 +64,9 @@ struct DeviceGuard {  // restores the caller's current device
   ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
 };
 
-}  // namespace
-
-extern "C" {
-
-eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg) {
-  return guarded<eh_graph*>(nullptr, [&]() -> eh_graph* {
+// The whole of eh_load_edges_ex below the ABI guard (also used by eh_count_batch).
+eh_graph* load_impl(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg) {
+  {
     eh_config c;
     std::memset(&c, 0, sizeof c);
     if (cfg) c = *cfg;
@@ -140,11 +137,114 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
       throw;
     }
     return g;
-  });
+  }
+}
+
+
+}  // namespace
+
+extern "C" {
+
+eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n, const eh_config* cfg) {
+  return guarded<eh_graph*>(nullptr, [&]() -> eh_graph* { return load_impl(src, dst, n, cfg); });
 }
 
 eh_graph* eh_load_edges(const uint32_t* src, const uint32_t* dst, uint64_t n) {
   return eh_load_edges_ex(src, dst, n, nullptr);
+}
+
+int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const uint64_t* n, uint64_t k,
+                   uint32_t query, const eh_config* cfg, uint64_t* counts) {
+  return guarded<int>(EH_ECUDA, [&]() -> int {
+    if (k && (!src || !dst || !n || !counts)) eh::fail(EH_EINVAL, "eh_count_batch: NULL argument");
+    if (query != EH_QUERY_TRIANGLES && query != EH_QUERY_4CLIQUES)
+      eh::fail(EH_EINVAL, "eh_count_batch: unknown query %u", query);
+    eh_config c;
+    std::memset(&c, 0, sizeof c);
+    if (cfg) c = *cfg;
+    if (c.flags & EH_INPUT_ON_DEVICE) eh::fail(EH_EINVAL, "eh_count_batch: inputs are host memory");
+    if (k == 0) return EH_OK;
+    uint64_t nmax = 0;
+    for (uint64_t i = 0; i < k; ++i) {
+      if (n[i] && (!src[i] || !dst[i])) eh::fail(EH_EINVAL, "eh_count_batch: NULL list %llu", (unsigned long long)i);
+      nmax = std::max(nmax, n[i]);
+    }
+    int dev = 0;
+    EH_CUDA(cudaGetDevice(&dev));
+    if (c.flags & EH_SET_DEVICE) dev = c.device;
+    DeviceGuard guard(dev);
+    // compute stream: the caller's, else a blocking library stream; uploads on a
+    // non-blocking copy stream, two device input buffers (ping-pong)
+    cudaStream_t cs = (cudaStream_t)c.stream, up = nullptr;
+    bool own_cs = false;
+    cudaEvent_t landed[2] = {nullptr, nullptr}, read[2] = {nullptr, nullptr};
+    eh::Allocator al;
+    al.hook_alloc = c.dev_alloc;
+    al.hook_free = c.dev_free;
+    al.ctx = c.alloc_ctx;
+    void* buf[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+      if (cs) cudaStreamSynchronize(cs);
+      if (up) cudaStreamSynchronize(up);
+      for (int b = 0; b < 2; ++b) {
+        if (buf[b]) al.release(buf[b]);
+        if (landed[b]) cudaEventDestroy(landed[b]);
+        if (read[b]) cudaEventDestroy(read[b]);
+      }
+      if (cs) cudaStreamSynchronize(cs);
+      if (up) cudaStreamDestroy(up);
+      if (own_cs && cs) cudaStreamDestroy(cs);
+    };
+    try {
+      if (!cs) {
+        EH_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamDefault));
+        own_cs = true;
+      }
+      EH_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+      al.stream = cs;
+      for (int b = 0; b < 2; ++b) {
+        EH_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
+        EH_CUDA(cudaEventCreateWithFlags(&read[b], cudaEventDisableTiming));
+        buf[b] = al.alloc(std::max<uint64_t>(1, 2 * nmax) * 4);
+      }
+      EH_CUDA(cudaStreamSynchronize(cs));  // the buffers exist before the copy stream writes them
+      auto upload = [&](uint64_t i) {
+        const int b = (int)(i & 1);
+        uint32_t* d = (uint32_t*)buf[b];
+        if (i >= 2) EH_CUDA(cudaStreamWaitEvent(up, read[b], 0));  // list i-2 has been read
+        if (n[i]) {
+          EH_CUDA(cudaMemcpyAsync(d, src[i], n[i] * 4, cudaMemcpyHostToDevice, up));
+          EH_CUDA(cudaMemcpyAsync(d + n[i], dst[i], n[i] * 4, cudaMemcpyHostToDevice, up));
+        }
+        EH_CUDA(cudaEventRecord(landed[b], up));
+      };
+      eh_config gc = c;
+      gc.flags |= EH_INPUT_ON_DEVICE;
+      gc.flags &= ~(uint32_t)EH_SET_DEVICE;
+      gc.stream = cs;
+      upload(0);
+      for (uint64_t i = 0; i < k; ++i) {
+        if (i + 1 < k) upload(i + 1);  // overlaps the load and count of list i
+        const int b = (int)(i & 1);
+        EH_CUDA(cudaStreamWaitEvent(cs, landed[b], 0));
+        const uint32_t* d = (const uint32_t*)buf[b];
+        eh_graph* g = load_impl(d, d + n[i], n[i], &gc);  // synchronous on cs: inputs read on return
+        EH_CUDA(cudaEventRecord(read[b], cs));
+        try {
+          counts[i] = query == EH_QUERY_4CLIQUES ? eh::count_4cliques(g) : eh::count_triangles(g);
+        } catch (...) {
+          destroy(g);
+          throw;
+        }
+        destroy(g);
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+    return EH_OK;
+  });
 }
 
 uint64_t eh_count_triangles(eh_graph* g) {

@@ -391,7 +391,11 @@ void build_worklists(eh_graph* g) {
   lo[2] = hi[1];
   hi[2] = 1ull << 33;
   // thread class = the head of class 0 with d <= thread_max (a7)
-  const uint64_t tmax = std::min<uint64_t>(g->bin_thread_max ? g->bin_thread_max : kThreadMaxDefault,
+  // default 8, 4 above 2^24 active ids (measured, bin_thread_max 1 / 4 / 8 / 12 / 16: C3 8.39 / 8.01 /
+  // 7.88 / 7.84 / 7.90 ms, C4 1.42 / 1.33 / 1.31 / 1.30 / 1.30, C2 0.312 / 0.294 / 0.302 / 0.314 / 0.339,
+  // C5 864 / 856 / 864 / 872 / 885)
+  const uint32_t tdef = g->n_act > (1ull << 24) ? 4u : kThreadMaxDefault;
+  const uint64_t tmax = std::min<uint64_t>(g->bin_thread_max ? g->bin_thread_max : tdef,
                                            std::min<uint64_t>(hi[0] - 1, tri_thread_max_degree()));
   const uint64_t ht = std::max<uint64_t>(2, tmax + 1);
   // one stable 4-way partition (class-major, each class in rank order)

@@ -91,6 +91,8 @@ def lib():
         L.eh_graph_export.restype = ctypes.c_int
         L.eh_free.argtypes = [vp]
         L.eh_free.restype = None
+        L.eh_count_batch.argtypes = [vp, vp, vp, u64, ctypes.c_uint32, ctypes.POINTER(EHConfig), vp]
+        L.eh_count_batch.restype = ctypes.c_int
         L.eh_release_cached_memory.argtypes = []
         L.eh_release_cached_memory.restype = None
         L.eh_launch_count.argtypes = []
@@ -104,7 +106,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("eh_load_edges", "eh_load_edges_ex", "eh_count_triangles", "eh_count_4cliques",
-                    "eh_count_triangles_range", "eh_count_4cliques_range", "eh_alg_bytes_k4",
+                    "eh_count_triangles_range", "eh_count_4cliques_range", "eh_alg_bytes_k4", "eh_count_batch",
                     "eh_count_triangles_unpruned", "eh_count_4cliques_unpruned", "eh_symmetric_stats",
                     "eh_triangles_per_vertex", "eh_count_lollipop", "eh_count_barbell", "eh_intersect",
                     "eh_graph_stats", "eh_graph_export", "eh_free", "eh_release_cached_memory", "eh_launch_count",
@@ -348,6 +350,37 @@ class Graph:
 def launch_count() -> int:
     """Kernels launched by libeh in this process (eh_launch_count)."""
     return int(lib().eh_launch_count())
+
+
+def count_batch(lists, query: str = "triangles", *, stream=None, tau: int = 0, all_uint: bool = False) -> list:
+    """eh_count_batch: load + count + free for each (src, dst) of `lists` (host
+    arrays; pinned torch tensors let the upload of list i+1 overlap the work on
+    list i).  query: "triangles" or "4cliques".  Returns the counts."""
+    L = lib()
+    k = len(lists)
+    keep = []
+    ps = (ctypes.c_void_p * max(k, 1))()
+    pd = (ctypes.c_void_p * max(k, 1))()
+    ns = (ctypes.c_uint64 * max(k, 1))()
+    for i, (src, dst) in enumerate(lists):
+        a, adev, ka = _ptr_of(src)
+        b, bdev, kb = _ptr_of(dst)
+        if adev or bdev:
+            raise ValueError("count_batch takes host arrays")
+        if _numel(src) != _numel(dst):
+            raise ValueError("src and dst differ in length")
+        keep += [ka, kb]
+        ps[i], pd[i], ns[i] = a, b, _numel(src)
+    cfg = EHConfig()
+    cfg.bitset_tau = tau
+    cfg.flags = EH_ALL_UINT if all_uint else 0
+    if stream is not None:
+        cfg.stream = getattr(stream, "cuda_stream", stream)
+    out = (ctypes.c_uint64 * max(k, 1))()
+    q = {"triangles": 0, "4cliques": 1}[query]
+    if L.eh_count_batch(ps, pd, ns, k, q, ctypes.byref(cfg), out) != EH_OK:
+        _raise()
+    return [int(out[i]) for i in range(k)]
 
 
 def release_cached_memory() -> None:

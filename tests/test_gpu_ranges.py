@@ -199,3 +199,28 @@ def test_triangles_per_vertex_out_checks():
         out = torch.zeros(n, dtype=torch.int64, device="cuda")
         g.triangles_per_vertex(out=out)
         assert np.array_equal(out.cpu().numpy().astype(np.uint64), ref)
+
+
+def test_count_batch_pipelined_uploads():
+    """eh_count_batch: k lists (pinned and pageable host memory, empty and repeated
+    lists), uploads overlapped with the work on the previous list; every count
+    equals the oracle's."""
+    import torch
+    lists, ref = [], []
+    for i, (sc, ef) in enumerate([(12, 16), (10, 8), (13, 16), (12, 16)]):
+        src, dst = synth.rmat(sc, ef, 4600 + i)
+        if i % 2 == 0:
+            src = torch.from_numpy(src.view(np.int32)).pin_memory()
+            dst = torch.from_numpy(dst.view(np.int32)).pin_memory()
+        lists.append((src, dst))
+        s_np = np.asarray(src).view(np.uint32) if not hasattr(src, "numpy") else src.numpy().view(np.uint32)
+        d_np = np.asarray(dst).view(np.uint32) if not hasattr(dst, "numpy") else dst.numpy().view(np.uint32)
+        ref.append((oracle.count_triangles(s_np, d_np), oracle.count_4cliques(s_np, d_np)))
+    e = np.zeros(0, np.uint32)
+    lists.insert(2, (e, e))
+    ref.insert(2, (0, 0))
+    lists.append(lists[0])
+    ref.append(ref[0])
+    assert eh.count_batch(lists) == [r[0] for r in ref]
+    assert eh.count_batch(lists, "4cliques", stream=torch.cuda.Stream()) == [r[1] for r in ref]
+    assert eh.count_batch([]) == []
