@@ -143,6 +143,10 @@ uint64_t* radix_sort_canon(const uint32_t* src, const uint32_t* dst, uint64_t n,
 // Sort segment v = data[off16[v]*4 .. + len[v]) in place for v < nseg (segsort.cu).
 void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
                         Allocator& al, cudaStream_t s);
+// Out of place: segment v = in[ioff[v] .. + len[v]) sorted into out[off16[v]*4 ..) (segments of one
+// element are copied; pads between output segments are left untouched).
+void segmented_sort_u32_into(const uint32_t* in, const uint64_t* ioff, uint32_t* out, const uint64_t* off16,
+                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s);
 // Same for u32 keys.
 uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s);

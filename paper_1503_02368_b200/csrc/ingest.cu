@@ -247,28 +247,12 @@ __global__ void k_level_fix(uint32_t* __restrict__ level, uint64_t n, uint32_t u
     if (level[i] == 0xFFFFFFFFu) level[i] = unreached;
 }
 
-// a5: orient low rank -> high rank: out-degree histogram of the low end.
-// Keys arrive sorted by their low id, so runs of equal low ends are common
-// inside a warp: atomics are aggregated over equal targets (__match_any_sync).
-__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
-                         const uint32_t* __restrict__ rank, uint32_t* __restrict__ dplus) {
-  const uint64_t mask = (1ull << b) - 1ull;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < m; base += stride) {
-    const uint64_t i = base + lane;
-    uint32_t lo = 0xFFFFFFFFu;
-    uint64_t k = 0;
-    if (i < m && key_head(keys, i, sentinel, k)) lo = min(rank[k >> b], rank[k & mask]);
-    const unsigned peers = __match_any_sync(kFull, lo);
-    if (lo != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&dplus[lo], (uint32_t)__popc(peers));
-  }
-}
-
-// a5: counting-sort scatter of the high end into the low end's padded list
-// (slot order within a list is arbitrary; segmented_sort_u32 orders it).  One
-// cursor atomic per group of equal low ends in the warp.
+// a5: counting-sort scatter of the high end into the low end's list (slot order
+// within a list is arbitrary; the segmented sort orders it).  One cursor atomic
+// per group of equal low ends in the warp.  kElem: list x starts at element
+// off[x] (the degree-capacity lists of build_trie, cursors end as |N+(x)|);
+// else at off[x] * 4 (padded 16-B offsets).
+template <bool kElem>
 __global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uint32_t b, uint64_t sentinel,
                               const uint32_t* __restrict__ rank, const uint64_t* __restrict__ off16,
                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ col) {
@@ -290,7 +274,7 @@ __global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uin
     uint32_t p0 = 0;
     if (lo != 0xFFFFFFFFu && lane == leader) p0 = atomicAdd(&cursor[lo], (uint32_t)__popc(peers));
     p0 = __shfl_sync(peers, p0, leader);
-    if (lo != 0xFFFFFFFFu) col[off16[lo] * 4 + p0 + __popc(peers & lt)] = hi;
+    if (lo != 0xFFFFFFFFu) col[off16[lo] * (kElem ? 1 : 4) + p0 + __popc(peers & lt)] = hi;
   }
 }
 
@@ -515,15 +499,25 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   mark("degree_rank");
 
   // ---- a5: orient + CSR (padded to 16 B per list)
-  // out-degree of the low end, padded 16-B list offsets, counting-sort scatter
-  // of the high end, then each list sorted in on-chip memory (segsort.cu).
+  // The high end (in rank order) of every edge is scattered into a temporary list
+  // of its low end with the low end's DEGREE as capacity (deg_rank, known since
+  // k_rank: no orientation pass has to count |N+(x)| first); the cursors end as
+  // |N+(x)|, which give the padded 16-B offsets of the final lists, and the
+  // segmented sort moves each list into place, in order (segsort.cu).
+  DBuf<uint64_t> toff(al, n_act + 1), tot(al, 1);
+  scan_exclusive_u32(g->deg_rank, toff.p, n_act, tot.p, al, s);
   DBuf<uint32_t> dplus(al, std::max<uint64_t>(1, n_act));
   EH_CUDA(cudaMemsetAsync(dplus.p, 0, std::max<uint64_t>(1, n_act) * 4, s));
+  DBuf<uint32_t> tmp(al, std::max<uint64_t>(1, 2 * m));
   if (m) {
-    k_orient<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, rank.p, dplus.p);
-    EH_LAUNCH("k_orient");
+    k_scatter_col<true><<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, rank.p, toff.p, dplus.p, tmp.p);
+    EH_LAUNCH("k_scatter_col");
   }
-  DBuf<uint64_t> off16(al, n_act + 1), tot(al, 1);
+  mark("scatter");
+  deg.reset();
+  keys.reset();  // the sorted keys are consumed
+  alt.reset();
+  DBuf<uint64_t> off16(al, n_act + 1);
   DBuf<uint32_t> p4(al, std::max<uint64_t>(1, n_act));
   k_pad4<<<grid_for(n_act, TB * 4), TB, 0, s>>>(dplus.p, n_act, p4.p);
   EH_LAUNCH("k_pad4");
@@ -544,14 +538,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   g->col = (uint32_t*)g->own(std::max<uint64_t>(16, total16 * 16));
   EH_CUDA(cudaMemsetAsync(g->col, 0xFF, std::max<uint64_t>(16, total16 * 16), s));
   mark("orient");
-  if (m) {
-    EH_CUDA(cudaMemsetAsync(p4.p, 0, std::max<uint64_t>(1, n_act) * 4, s));  // reuse as cursors
-    k_scatter_col<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, rank.p, off16.p, p4.p, g->col);
-    EH_LAUNCH("k_scatter_col");
-  }
-  deg.reset();
-  mark("scatter");
-  segmented_sort_u32(g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s);
+  segmented_sort_u32_into(tmp.p, toff.p, g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s);
   mark("segsort");
   g->desc = (uint4*)g->own((n_act + 1) * sizeof(uint4));
   k_desc_base<<<grid_for(n_act + 1, TB * 4), TB, 0, s>>>(off16.p, dplus.p, n_act, total16, g->desc);

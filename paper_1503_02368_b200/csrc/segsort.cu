@@ -1,5 +1,5 @@
-// segsort.cu -- sort many short u32 segments in place (SURVEY.md §8(a) row a5:
-// "CSR with strictly increasing out-lists").
+// segsort.cu -- sort many short u32 segments, in place or into another layout
+// ("CSR with strictly increasing out-lists").
 //
 // After orientation the out-lists are filled by a counting-sort scatter (atomic
 // cursor per list), which leaves each list in arbitrary order.  Degree
@@ -26,8 +26,13 @@ constexpr int kMidMax = 1024;  // register tiers up to here (E = 32 keys per lan
 constexpr int kBigMax = 8192, kBigThreads = 1024;
 
 struct Seg {
-  const uint64_t* off16;  // segment v starts at element off16[v] * 4
+  const uint64_t* off16;  // output segment v starts at element off16[v] * 4
   const uint32_t* len;
+  const uint32_t* in;     // out-of-place: input segment v at in + ioff[v] (else in place)
+  const uint64_t* ioff;
+  __device__ __forceinline__ const uint32_t* src(uint32_t* data, uint32_t v) const {
+    return ioff ? in + ioff[v] : data + off16[v] * 4;
+  }
 };
 
 // Bitonic network over 32 * E keys held E per lane (key index e * 32 + lane, so
@@ -73,11 +78,12 @@ __global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* 
     const uint32_t v = ids[t];
     const uint32_t n = sg.len[v];
     uint32_t* p = data + sg.off16[v] * 4;
+    const uint32_t* q = sg.src(data, v);
     uint32_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t i = e * 32 + lane;
-      x[e] = (i < n) ? p[i] : kPad;
+      x[e] = (i < n) ? q[i] : kPad;
     }
     warp_bitonic_regs<E>(x, lane);
 #pragma unroll
@@ -114,12 +120,14 @@ __device__ __forceinline__ void sort_group(uint32_t* __restrict__ data, const Se
   const int sl = lane & (S - 1);
   uint32_t n = 0;
   uint32_t* p = nullptr;
+  const uint32_t* q = nullptr;
   if (t < nids) {
     const uint32_t v = ids[t];
     n = sg.len[v];
     p = data + sg.off16[v] * 4;
+    q = sg.src(data, v);
   }
-  uint32_t x = ((uint32_t)sl < n) ? p[sl] : kPad;
+  uint32_t x = ((uint32_t)sl < n) ? q[sl] : kPad;
   x = subwarp_bitonic<S>(x, lane);
   if ((uint32_t)sl < n) p[sl] = x;
 }
@@ -173,9 +181,10 @@ __global__ void __launch_bounds__(kBigThreads) k_seg_big(uint32_t* __restrict__ 
     const uint32_t v = ids[t];
     const uint32_t n = sg.len[v];
     uint32_t* p = data + sg.off16[v] * 4;
+    const uint32_t* q = sg.src(data, v);
     uint32_t N = 2048;
     while (N < n) N <<= 1;
-    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? p[i] : kPad;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? q[i] : kPad;
     __syncthreads();
     bitonic_smem<true>(s, N, threadIdx.x, blockDim.x);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) p[i] = s[i];
@@ -184,12 +193,12 @@ __global__ void __launch_bounds__(kBigThreads) k_seg_big(uint32_t* __restrict__ 
 }
 
 // ---- fallback for segments longer than kBigMax ----
-__global__ void k_seg_gather(const uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids,
+__global__ void k_seg_gather(uint32_t* __restrict__ data, Seg sg, const uint32_t* __restrict__ ids,
                              uint64_t nids, const uint64_t* __restrict__ goff, uint64_t* __restrict__ keys) {
   for (uint64_t t = blockIdx.x; t < nids; t += gridDim.x) {
     const uint32_t v = ids[t];
     const uint32_t n = sg.len[v];
-    const uint32_t* p = data + sg.off16[v] * 4;
+    const uint32_t* p = sg.src(data, v);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[goff[t] + i] = (t << 32) | p[i];
   }
 }
@@ -206,9 +215,10 @@ __global__ void k_seg_scatter(uint32_t* __restrict__ data, Seg sg, const uint32_
 // tier of a segment by its length (-1: nothing to sort), tiers as in segmented_sort_u32
 struct TierOf {
   const uint32_t* len;
+  uint32_t min_len;  // 2 in place; 1 out of place (single elements are copied)
   __device__ int operator()(uint64_t v) const {
     const uint32_t n = len[v];
-    if (n < 2) return -1;
+    if (n < min_len) return -1;
     if (n <= 32) return 0;
     if (n <= 64) return 1;
     if (n <= 128) return 2;
@@ -231,16 +241,15 @@ __global__ void k_gather_len(const uint32_t* __restrict__ len, const uint32_t* _
 
 }  // namespace
 
-void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
-                        Allocator& al, cudaStream_t s) {
-  if (nseg == 0 || max_len <= 1) return;
-  const Seg sg{off16, len};
+static void segsort_impl(uint32_t* data, const Seg& sg, uint64_t nseg, uint32_t max_len, Allocator& al,
+                         cudaStream_t s) {
+  const uint32_t* len = sg.len;
   DBuf<uint32_t> all_ids(al, nseg);
   DBuf<uint64_t> starts(al, 10);  // one partition of the segments by tier, kept on the device:
-  partition_k_async<8>(nseg, TierOf{len}, TierEmit{all_ids.p}, starts.p, al, s);  // no host sync
+  partition_k_async<8>(nseg, TierOf{len, sg.ioff ? 1u : 2u}, TierEmit{all_ids.p}, starts.p, al, s);  // no host sync
   // the tier kernels read their range from `starts`; grids are sized for the worst
   // case the host knows (nseg, max_len) and stride over what is there
-  const uint32_t tier_min[8] = {2, 33, 65, 129, 257, 513, (uint32_t)kMidMax + 1, (uint32_t)kBigMax + 1};
+  const uint32_t tier_min[8] = {1, 33, 65, 129, 257, 513, (uint32_t)kMidMax + 1, (uint32_t)kBigMax + 1};
   for (int tier = 0; tier < 7; ++tier) {
     if (max_len < tier_min[tier]) break;
     const uint64_t* rng = starts.p + tier;
@@ -278,6 +287,18 @@ void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* l
       EH_CUDA(cudaStreamSynchronize(s));  // temporaries are released on return
     }
   }
+}
+
+void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
+                        Allocator& al, cudaStream_t s) {
+  if (nseg == 0 || max_len <= 1) return;
+  segsort_impl(data, Seg{off16, len, nullptr, nullptr}, nseg, max_len, al, s);
+}
+
+void segmented_sort_u32_into(const uint32_t* in, const uint64_t* ioff, uint32_t* out, const uint64_t* off16,
+                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s) {
+  if (nseg == 0 || max_len == 0) return;
+  segsort_impl(out, Seg{off16, len, in, ioff}, nseg, max_len, al, s);
 }
 
 }  // namespace eh
