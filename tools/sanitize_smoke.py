@@ -39,6 +39,25 @@ s, d = synth.complete(1100)                       # |N+(x)| > 1024: K4 fallback 
 with eh.Graph(s, d) as g:
     assert g.count_triangles() == comb(1100, 3)
     assert g.count_4cliques() == comb(1100, 4)
+# NEXT rows, rank ranges, thread class, TMA-staged wide triangle kernels, the batch API
+og = oracle.Graph(src, dst)
+with eh.Graph(src, dst) as g:
+    n = g.stats().n_active
+    assert g.count_triangles_range(0, n // 2) == og.count_triangles_rank_range(0, n // 2)
+    assert g.count_4cliques_range(n // 2, n) == og.count_4cliques_rank_range(n // 2, n)
+    assert g.count_lollipop() == og.count_lollipop() and g.count_barbell() == og.count_barbell()
+    assert g.count_triangles_unpruned() == og.count_triangles_unpruned()
+    assert g.count_4cliques_unpruned() == og.count_4cliques_unpruned()
+    g.alg_bytes_k4()
+T = og.count_triangles()
+with eh.Graph(src, dst, block_layout=True, order="bfs", bin_thread_max=16) as g:
+    assert g.count_triangles() == T
+os.environ["EH_TEST_TRI_WIDE"] = "1"
+with eh.Graph(src, dst) as g:
+    assert g.count_triangles() == T
+del os.environ["EH_TEST_TRI_WIDE"]
+assert eh.count_batch([(src, dst), (src[:1000], dst[:1000]), (src, dst)])[0] == T
+og.close()
 e = np.zeros(0, np.uint32)
 with eh.Graph(e, e) as g:
     assert g.count_triangles() == 0 and g.count_4cliques() == 0
