@@ -23,7 +23,10 @@ with torch.cuda.stream(st):
     g = eh.Graph(s, d, stream=st)
     ref = None
     for val in sys.argv[3:]:
-        os.environ[var] = val
+        if val == "-":
+            os.environ.pop(var, None)  # "-": the variable unset
+        else:
+            os.environ[var] = val
         ts = []
         for r in range(6):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
