@@ -475,6 +475,21 @@ uint64_t k4_impl(eh_graph* g) {
   const uint64_t nsmall = g->n_work[0] + g->n_work[1];  // d <= tri_warp_max_degree() = kWMaxD
   const uint64_t nlarge = g->n_work[2];
   const uint32_t* wl = work_lpt(g) + nsmall;  // class 2 heaviest first
+  // the warp-class kernel runs on a side stream beside the CTA-class kernels (they
+  // share only the count, an atomic); test hook EH_TEST_K4_SERIAL keeps one stream
+  // (EH_TEST_K4_SHAPES=1: the three CTA shapes on streams of their own as well)
+  const bool serial = getenv("EH_TEST_K4_SERIAL") != nullptr;
+  const bool shapes = !serial && getenv("EH_TEST_K4_SHAPES") != nullptr;
+  const cudaStream_t ss = (!serial && nsmall && nlarge) ? fork_side(g, 0) : s;
+  const cudaStream_t s1 = (shapes && nlarge) ? fork_side(g, 1) : s;
+  const cudaStream_t s2 = (shapes && nlarge && g->max_dplus > 512) ? fork_side(g, 2) : s;
+  if (nsmall) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
+    const size_t smem = sizeof(K4WarpSmem) * kWWarps;
+    EH_CUDA(cudaFuncSetAttribute(k_k4_warp<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_k4_warp<kU><<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter, sf16);
+    EH_LAUNCH("k_k4_warp");
+  }
   if (nlarge) {
     // d <= 256: 4-warp CTAs (~20 KB); d <= 512: 8-warp CTAs (~57 KB); 512 < d <= 1024: 16 warps, ~190 KB
     {
@@ -494,7 +509,7 @@ uint64_t k4_impl(eh_graph* g) {
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 8 * 32, sm1));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k1<<<grid, 8 * 32, sm1, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u, sf16);
+      k1<<<grid, 8 * 32, sm1, s1>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u, sf16);
       EH_LAUNCH("k_k4_cta");
     }
     if (g->max_dplus > 512) {
@@ -502,7 +517,7 @@ uint64_t k4_impl(eh_graph* g) {
       auto k2 = k_k4_cta<kU, kCMaxD, 16>;
       EH_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
       const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-      k2<<<grid, 16 * 32, sm2, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u, sf16);
+      k2<<<grid, 16 * 32, sm2, s2>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u, sf16);
       EH_LAUNCH("k_k4_cta");
     }
     if (g->max_dplus > (uint64_t)kCMaxD) {
@@ -528,13 +543,9 @@ uint64_t k4_impl(eh_graph* g) {
       EH_CUDA(cudaStreamSynchronize(s));  // scratch is released on return
     }
   }
-  if (nsmall) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
-    const size_t smem = sizeof(K4WarpSmem) * kWWarps;
-    EH_CUDA(cudaFuncSetAttribute(k_k4_warp<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_k4_warp<kU><<<grid, kWWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter, sf16);
-    EH_LAUNCH("k_k4_warp");
-  }
+  if (ss != s) join_side(g, 0);
+  if (s1 != s) join_side(g, 1);
+  if (s2 != s) join_side(g, 2);
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   return g->h_counter[0];

@@ -504,12 +504,12 @@ __global__ void __launch_bounds__(kTBlock) k_tri_thread(const uint4* __restrict_
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
-void launch_thread(eh_graph* g, uint64_t nt) {
+void launch_thread(eh_graph* g, uint64_t nt, cudaStream_t st) {
   if (nt == 0) return;
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_thread, kTBlock, 0));
   const unsigned grid = (unsigned)std::min<uint64_t>((nt + kTBlock - 1) / kTBlock, (uint64_t)kSMs * std::max(1, per_sm));
-  k_tri_thread<<<grid, kTBlock, 0, g->stream>>>(g->desc, g->col, g->bs, g->work, nt, g->d_counter);
+  k_tri_thread<<<grid, kTBlock, 0, st>>>(g->desc, g->col, g->bs, g->work, nt, g->d_counter);
   EH_LAUNCH("k_tri_thread");
 }
 
@@ -803,7 +803,9 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
 
 
 template <bool kUnpruned, bool kBlock, int kMaxD, int kMinB, int kWG = kG, uint32_t kSF = 64, bool kPiv = false>
-void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, uint32_t cslot = 1) {
+void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, uint32_t cslot = 1,
+                 cudaStream_t st = nullptr) {
+  if (!st) st = g->stream;
   if (nsmall == 0) return;
   if (!work) work = g->work;
   auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF, kPiv>;
@@ -813,7 +815,7 @@ void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, u
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWK_Warps * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps,
                                                      (uint64_t)kSMs * std::max(1, per_sm));
-  k<<<grid, kWK_Warps * 32, smem, g->stream>>>(g->desc, g->col, g->bs, work, nsmall, g->d_counter,
+  k<<<grid, kWK_Warps * 32, smem, st>>>(g->desc, g->col, g->bs, work, nsmall, g->d_counter,
                                                BlockView{g->bdesc, g->bcol, g->bcid, g->bmask}, cslot);
   EH_LAUNCH("k_tri_warp");
 }
@@ -829,6 +831,32 @@ uint64_t count_impl(eh_graph* g) {
   const bool wide = g->n_act > kWideIds || kUnpruned || getenv("EH_TEST_TRI_WIDE") != nullptr;
   const uint64_t nsmall = g->n_work[0] + (wide ? g->n_work[1] : 0);
   const uint64_t nlarge = g->n_work[2] + (wide ? 0 : g->n_work[1]);
+  // The thread- and warp-class kernels run on a side stream beside the CTA-class
+  // kernel (they share only the count, an atomic), so the tail of one overlaps the
+  // other; test hook EH_TEST_TRI_SERIAL keeps one stream.
+  const cudaStream_t ss = getenv("EH_TEST_TRI_SERIAL") == nullptr ? fork_side(g, 0) : s;
+  // a7 thread class (the head of class 0; pruned set-level nest only)
+  const uint64_t nt = (!kUnpruned && !kBlock) ? g->n_thread : 0;
+  launch_thread(g, nt, ss);
+  if (nsmall > nt) {
+    // staging sized for class 0 (|N+(x)| <= 64 by default): 30 KB instead of 43 KB
+    // per 8-warp CTA, one more CTA per SM (measured: C3 9.48 -> 9.41 ms)
+    // SEARCH rows start inside one of 8 pivot slices on the larger graphs (> 2^20 active
+    // ids; measured C3 9.15 -> 8.92 ms, C5 900 -> 887; slower on C2 / C4)
+    const bool big = g->n_act > (1ull << 20);
+    // min 6 CTAs per SM: 40 registers (a few spilled bytes) for one more resident CTA
+    // (measured C3 8.59 -> 8.38 ms, C4 1.458 -> 1.419, C2 0.316 -> 0.313)
+    const uint32_t* w0 = g->work + nt;
+    const uint64_t n0 = nsmall - nt;
+    if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16, true>(g, n0, w0, 1u, ss);
+    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, n0, w0, 1u, ss);
+    else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, n0, w0, 1u, ss);
+    else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, n0, w0, 1u, ss);
+    else if (!kUnpruned && !kBlock && g->class0_max <= 64) {  // wide: class 0 with 64-entry staging, min 6 CTAs/SM
+      launch_warp<kUnpruned, kBlock, 64, 6, kG, 64, true>(g, g->n_work[0] - nt, w0, 1u, ss);
+      launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall - g->n_work[0], g->work + g->n_work[0], 6u, ss);
+    } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, n0, w0, 1u, ss);
+  }
   if (nlarge) {
     // unpruned: lists above 4096 use the global hub bitmaps (measured: C3 0.93 -> 0.42 s)
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
@@ -846,28 +874,7 @@ uint64_t count_impl(eh_graph* g) {
     else if (g->n_act <= (1ull << 20)) launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, 4, 16>(g, nsmall, nlarge, xcap);
     else launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, xcap);
   }
-  // a7 thread class (the head of class 0; pruned set-level nest only)
-  const uint64_t nt = (!kUnpruned && !kBlock) ? g->n_thread : 0;
-  launch_thread(g, nt);
-  if (nsmall > nt) {
-    // staging sized for class 0 (|N+(x)| <= 64 by default): 30 KB instead of 43 KB
-    // per 8-warp CTA, one more CTA per SM (measured: C3 9.48 -> 9.41 ms)
-    // SEARCH rows start inside one of 8 pivot slices on the larger graphs (> 2^20 active
-    // ids; measured C3 9.15 -> 8.92 ms, C5 900 -> 887; slower on C2 / C4)
-    const bool big = g->n_act > (1ull << 20);
-    // min 6 CTAs per SM: 40 registers (a few spilled bytes) for one more resident CTA
-    // (measured C3 8.59 -> 8.38 ms, C4 1.458 -> 1.419, C2 0.316 -> 0.313)
-    const uint32_t* w0 = g->work + nt;
-    const uint64_t n0 = nsmall - nt;
-    if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16, true>(g, n0, w0);
-    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, n0, w0);
-    else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, n0, w0);
-    else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, n0, w0);
-    else if (!kUnpruned && !kBlock && g->class0_max <= 64) {  // wide: class 0 with 64-entry staging, min 6 CTAs/SM
-      launch_warp<kUnpruned, kBlock, 64, 6, kG, 64, true>(g, g->n_work[0] - nt, w0, 1u);
-      launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall - g->n_work[0], g->work + g->n_work[0], 6u);
-    } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, n0, w0);
-  }
+  if (ss != s) join_side(g, 0);
   EH_CUDA(cudaMemcpyAsync(g->h_counter, g->d_counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   EH_CUDA(cudaStreamSynchronize(s));
   return g->h_counter[0];

@@ -38,6 +38,16 @@ R guarded(R on_error, F&& f) {
   return on_error;
 }
 
+void release_sides(eh_graph* g) {
+  for (int k = 0; k < eh_graph::kSides; ++k)
+    if (g->side[k]) {
+      cudaStreamSynchronize(g->side[k]);
+      cudaStreamDestroy(g->side[k]);
+      cudaEventDestroy(g->ev_join[k]);
+    }
+  if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+}
+
 void destroy(eh_graph* g) {
   if (!g) return;
   int prev = -1;
@@ -45,9 +55,12 @@ void destroy(eh_graph* g) {
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->sym) {
-    for (void* p : g->sym->owned) g->sym->alloc.release(p);
-    delete g->sym;
+    eh_graph* h = g->sym;
+    release_sides(h);
+    for (void* p : h->owned) h->alloc.release(p);
+    delete h;
   }
+  release_sides(g);
   for (void* p : g->owned) g->alloc.release(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);

@@ -244,6 +244,10 @@ struct eh_graph {
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
   eh_graph* sym = nullptr;  // NEXT-2: symmetric (unpruned) trie, built on first use (sym.cu)
+  // side streams + fork / join events of the count kernels (created on first use)
+  static constexpr int kSides = 3;
+  cudaStream_t side[kSides] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kSides] = {};
 
   std::vector<void*> owned;  // every device allocation above
   uint64_t device_bytes = 0;
@@ -282,6 +286,23 @@ class WorkRange {
   uint64_t saved_n_[3], saved_nt_;
   DBuf<uint32_t> work_, lpt_;
 };
+// Fork: side stream k of the handle (non-blocking, created on first use) waits for
+// the work queued so far on the handle's stream.  Join: the handle's stream waits
+// for everything queued on side stream k.
+inline cudaStream_t fork_side(eh_graph* g, int k) {
+  if (!g->ev_fork) EH_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+  if (!g->side[k]) {
+    EH_CUDA(cudaStreamCreateWithFlags(&g->side[k], cudaStreamNonBlocking));
+    EH_CUDA(cudaEventCreateWithFlags(&g->ev_join[k], cudaEventDisableTiming));
+  }
+  EH_CUDA(cudaEventRecord(g->ev_fork, g->stream));
+  EH_CUDA(cudaStreamWaitEvent(g->side[k], g->ev_fork, 0));
+  return g->side[k];
+}
+inline void join_side(eh_graph* g, int k) {
+  EH_CUDA(cudaEventRecord(g->ev_join[k], g->side[k]));
+  EH_CUDA(cudaStreamWaitEvent(g->stream, g->ev_join[k], 0));
+}
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);
 uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept
