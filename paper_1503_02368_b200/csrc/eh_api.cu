@@ -22,6 +22,11 @@ void set_status(int code, const char* msg) {
 }
 void ok() { set_status(EH_OK, ""); }
 
+// int-returning entry points: the EH_E* status of the failure itself (EH_EINVAL,
+// EH_ENOMEM, EH_ECUDA), not a fixed code
+template <class F>
+int guarded_status(F&& f);
+
 template <class R, class F>
 R guarded(R on_error, F&& f) {
   try {
@@ -46,6 +51,12 @@ void release_sides(eh_graph* g) {
       cudaEventDestroy(g->ev_join[k]);
     }
   if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+}
+
+template <class F>
+int guarded_status(F&& f) {
+  const int r = guarded<int>(INT32_MIN, std::forward<F>(f));
+  return r == INT32_MIN ? t_status : r;
 }
 
 void destroy(eh_graph* g) {
@@ -168,7 +179,7 @@ eh_graph* eh_load_edges(const uint32_t* src, const uint32_t* dst, uint64_t n) {
 
 int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const uint64_t* n, uint64_t k,
                    uint32_t query, const eh_config* cfg, uint64_t* counts) {
-  return guarded<int>(EH_ECUDA, [&]() -> int {
+  return guarded_status([&]() -> int {
     if (k && (!src || !dst || !n || !counts)) eh::fail(EH_EINVAL, "eh_count_batch: NULL argument");
     if (query != EH_QUERY_TRIANGLES && query != EH_QUERY_4CLIQUES)
       eh::fail(EH_EINVAL, "eh_count_batch: unknown query %u", query);
@@ -182,9 +193,14 @@ int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const
       if (n[i] && (!src[i] || !dst[i])) eh::fail(EH_EINVAL, "eh_count_batch: NULL list %llu", (unsigned long long)i);
       nmax = std::max(nmax, n[i]);
     }
-    int dev = 0;
+    int dev = 0, ndev = 0;
+    EH_CUDA(cudaGetDeviceCount(&ndev));
+    if (ndev <= 0) eh::fail(EH_ECUDA, "no CUDA device");
     EH_CUDA(cudaGetDevice(&dev));
-    if (c.flags & EH_SET_DEVICE) dev = c.device;
+    if (c.flags & EH_SET_DEVICE) {
+      if (c.device < 0 || c.device >= ndev) eh::fail(EH_EINVAL, "eh_count_batch: bad device %d", c.device);
+      dev = c.device;
+    }
     DeviceGuard guard(dev);
     // compute stream: the caller's, else a blocking library stream; uploads on a
     // non-blocking copy stream, two device input buffers (ping-pong)
@@ -320,7 +336,7 @@ uint64_t eh_count_4cliques_unpruned(eh_graph* g) {
 }
 
 int eh_symmetric_stats(eh_graph* g, eh_stats* out) {
-  return guarded<int>(EH_ECUDA, [&]() -> int {
+  return guarded_status([&]() -> int {
     if (!g || !out) eh::fail(EH_EINVAL, "eh_symmetric_stats: NULL argument");
     DeviceGuard guard(g->device);
     eh_graph* h = eh::symmetric_trie(g);
@@ -339,7 +355,7 @@ int eh_symmetric_stats(eh_graph* g, eh_stats* out) {
 }
 
 int eh_triangles_per_vertex(eh_graph* g, uint64_t* t) {
-  return guarded<int>(EH_ECUDA, [&]() -> int {
+  return guarded_status([&]() -> int {
     if (!g || (!t && g->n_act)) eh::fail(EH_EINVAL, "eh_triangles_per_vertex: NULL argument");
     DeviceGuard guard(g->device);
     if (g->n_act == 0) return EH_OK;
@@ -362,7 +378,7 @@ int eh_triangles_per_vertex(eh_graph* g, uint64_t* t) {
 }
 
 static int count128(eh_graph* g, uint64_t* out, bool barbell, const char* what) {
-  return guarded<int>(EH_ECUDA, [&]() -> int {
+  return guarded_status([&]() -> int {
     if (!g || !out) eh::fail(EH_EINVAL, "%s: NULL argument", what);
     DeviceGuard guard(g->device);
     eh::count_lollipop_barbell(g, barbell, out);
@@ -383,7 +399,7 @@ int eh_graph_stats(const eh_graph* g, eh_stats* out) {
     set_status(EH_EINVAL, "eh_graph_stats: NULL argument");
     return EH_EINVAL;
   }
-  const int rc = guarded<int>(EH_ECUDA, [&]() -> int {
+  const int rc = guarded_status([&]() -> int {
     DeviceGuard guard(g->device);
     eh::compute_stats(const_cast<eh_graph*>(g));  // cached, logically const
     return EH_OK;
@@ -403,7 +419,7 @@ int eh_graph_stats(const eh_graph* g, eh_stats* out) {
 }
 
 int eh_graph_export(const eh_graph* g, uint64_t* row_ptr, uint32_t* col, uint32_t* orig_id, uint8_t* is_bitset) {
-  return guarded<int>(EH_ECUDA, [&]() -> int {
+  return guarded_status([&]() -> int {
     if (!g) eh::fail(EH_EINVAL, "eh_graph_export: NULL graph");
     DeviceGuard guard(g->device);
     const uint64_t n = g->n_act;

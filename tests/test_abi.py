@@ -69,6 +69,24 @@ def test_argument_errors_without_device_work():
     cfg.flags = 0x80
     assert L.eh_load_edges_ex(None, None, 0, ctypes.byref(cfg)) is None and L.eh_last_status() == eh.EH_EINVAL
     assert b"flags" in L.eh_last_error()
+    # eh_count_batch: argument checks precede any device work
+    cnt = (ctypes.c_uint64 * 1)()
+    assert L.eh_count_batch(None, None, None, 1, 0, None, cnt) == eh.EH_EINVAL
+    arr = (ctypes.c_void_p * 1)()
+    ns = (ctypes.c_uint64 * 1)(0)
+    assert L.eh_count_batch(arr, arr, ns, 1, 7, None, cnt) == eh.EH_EINVAL and b"query" in L.eh_last_error()
+    cfg.flags = eh.EH_INPUT_ON_DEVICE
+    assert L.eh_count_batch(arr, arr, ns, 1, 0, ctypes.byref(cfg), cnt) == eh.EH_EINVAL
+    assert L.eh_count_triangles_range(None, 0, 1) == eh.EH_COUNT_ERROR and L.eh_last_status() == eh.EH_EINVAL
+    assert L.eh_count_4cliques_range(None, 0, 1) == eh.EH_COUNT_ERROR and L.eh_last_status() == eh.EH_EINVAL
+    assert L.eh_alg_bytes_k4(None) == eh.EH_COUNT_ERROR and L.eh_last_status() == eh.EH_EINVAL
+    L.eh_release_cached_memory()  # safe with nothing cached (and without a device)
+    # int-returning calls report the status of the failure itself
+    out2 = (ctypes.c_uint64 * 2)()
+    assert L.eh_count_lollipop(None, out2) == eh.EH_EINVAL and L.eh_count_barbell(None, out2) == eh.EH_EINVAL
+    assert L.eh_triangles_per_vertex(None, None) == eh.EH_EINVAL
+    assert L.eh_symmetric_stats(None, None) == eh.EH_EINVAL
+    assert L.eh_graph_export(None, None, None, None, None) == eh.EH_EINVAL
 
 
 def _has_cuda():
