@@ -46,14 +46,22 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
-    """Compile every csrc/*.cu to an object (in parallel) and link libeh.so."""
+SO_CHECKED = os.path.join(LIBDIR, "libeh_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None, checked: bool = False) -> str:
+    """Compile every csrc/*.cu to an object (in parallel) and link libeh.so.
+
+    checked=True builds lib/libeh_checked.so instead: the same sources with
+    -DEH_CHECKED, i.e. the device-side bounds assertions of csrc/check.cuh live
+    (the test suite's substitute for compute-sanitizer, closed on this pool)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    stamp = os.path.join(LIBDIR, "libeh.sha256")
+    so = SO_CHECKED if checked else SO
+    stamp = os.path.join(LIBDIR, "libeh_checked.sha256" if checked else "libeh.sha256")
     dig = _digest()
-    if not force and os.path.exists(SO) and os.path.exists(stamp) and open(stamp).read().strip() == dig:
-        return SO
-    objdir = os.path.join(LIBDIR, "obj")
+    if not force and os.path.exists(so) and os.path.exists(stamp) and open(stamp).read().strip() == dig:
+        return so
+    objdir = os.path.join(LIBDIR, "obj_checked" if checked else "obj")
     os.makedirs(objdir, exist_ok=True)
     cc = nvcc()
     procs = []
@@ -61,7 +69,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     for src in _sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *(["-DEH_CHECKED"] if checked else []), "-I", INCLUDE, "-I", CSRC,
+               "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -76,13 +85,13 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     if failed:
         msg = "\n".join(f"--- {s}\n{t}" for s, t in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = SO + f".tmp{os.getpid()}"
+    tmp = so + f".tmp{os.getpid()}"
     subprocess.check_call([cc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, SO)
+    os.replace(tmp, so)
     with open(stamp, "w") as f:
         f.write(dig)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

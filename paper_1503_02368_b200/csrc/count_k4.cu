@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
     const uint32_t x = __ldg(work + wi);
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;  // 2 <= d <= kWMaxD
+    EH_DASSERT(d >= 2 && d <= (uint32_t)kWMaxD);
     if (d < 3) continue;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
       const uint32_t incl = warp_inclusive_scan(c);
       const uint32_t ne = __shfl_sync(kFull, incl, 31);
       uint32_t p = incl - c, t = wv;
+      EH_DASSERT(incl <= d);
       while (t) {
         const uint32_t b = __ffs(t) - 1;
         t &= t - 1;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(kBigThreads) k_k4_big(const uint4* __restrict_
     const uint32_t nsrc = stream_a ? d - a0 : sy.len;
     const uint32_t* src = stream_a ? xs + a0 : sy.list;
     uint32_t* P = (min(d - a0, sy.len) <= kBigPCap) ? Psm : Pglob;
+    EH_DASSERT(min(d - a0, sy.len) <= pstride);
     uint32_t np = 0;
     for (uint32_t j0 = 0; j0 < nsrc; j0 += kBigThreads) {
       const uint32_t j = j0 + threadIdx.x;

@@ -105,6 +105,7 @@ __device__ __forceinline__ XSet plan_xset(uint32_t* tab, uint32_t tab_words, con
   uint32_t hbits = 5;  // smallest table >= 8d that fits the budget
   while ((1u << hbits) < 8 * d && (2u << hbits) <= tab_words) ++hbits;
   if (span_bits <= 32ull * tab_words) {
+    EH_DASSERT(d >= 1 && s.amin <= s.amax);
     s.mode = kBitmap;
     s.lo = lo;
     s.nbits = (uint32_t)span_bits;
@@ -136,6 +137,7 @@ __device__ __forceinline__ void fill_xset(const XSet& s, int tid, int nthreads) 
   if (s.mode == kBitmap) {
     for (uint32_t k = tid; k < d; k += nthreads) {
       const uint32_t o = xs[k] - lo;
+      EH_DASSERT(o < s.nbits);
       atomicOr(&tab[o >> 5], 1u << (o & 31));
     }
   } else if (s.mode == kHash) {
@@ -217,6 +219,7 @@ __device__ __forceinline__ uint32_t grp_row(uint8_t kd, const uint32_t* __restri
     const uint32_t lo = max(y.c0, xc0), hi = min(y.c1, xc1);
     const uint4* yb = reinterpret_cast<const uint4*>(bs) + y.pool;  // chunk y.c0
     const uint4* xb = reinterpret_cast<const uint4*>(X.tab);        // chunk xc0
+    EH_DASSERT(X.mode == kBitmap && lo >= y.c0 && hi <= y.c1 && lo >= xc0 && hi <= xc1);
     uint32_t k = lo + gl;                                            // absolute chunk index
     if (kAndU == 4) {  // 4 chunk loads in flight per lane (narrow shape on large graphs: C3 8.90 -> 8.63 ms)
       for (; k + 3 * G < hi; k += 4 * G) {
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(kWK_Warps * 32, kMinB) k_tri_warp(const uint4*
     const uint32_t x = __ldg(work + wi);
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;  // 2 <= d <= kWarpMaxD
+    EH_DASSERT(d >= 2 && d <= (uint32_t)kMaxD);
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
@@ -471,6 +475,7 @@ __global__ void __launch_bounds__(kTBlock) k_tri_thread(const uint4* __restrict_
     const uint32_t x = __ldg(work + k);
     const uint4 dx = __ldg(desc + x);
     const uint32_t d = dx.y;  // 2 <= d <= kTMax
+    EH_DASSERT(d >= 2 && d <= (uint32_t)kTMax);
     const uint4* xg = reinterpret_cast<const uint4*>(col) + dx.x;
     for (uint32_t q = 0; q < (d + 3) / 4; ++q) {
       const uint4 v = __ldg(xg + q);

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "check.cuh"
 #include "eh.h"
 
 namespace eh {

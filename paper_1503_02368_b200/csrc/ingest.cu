@@ -274,6 +274,7 @@ __global__ void k_scatter_col(const uint64_t* __restrict__ keys, uint64_t m, uin
     uint32_t p0 = 0;
     if (lo != 0xFFFFFFFFu && lane == leader) p0 = atomicAdd(&cursor[lo], (uint32_t)__popc(peers));
     p0 = __shfl_sync(peers, p0, leader);
+    EH_DASSERT(lo == 0xFFFFFFFFu || !kElem || off16[lo] + p0 + __popc(peers & lt) < off16[lo + 1]);
     if (lo != 0xFFFFFFFFu) col[off16[lo] * (kElem ? 1 : 4) + p0 + __popc(peers & lt)] = hi;
   }
 }
@@ -506,6 +507,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   // segmented sort moves each list into place, in order (segsort.cu).
   DBuf<uint64_t> toff(al, n_act + 1), tot(al, 1);
   scan_exclusive_u32(g->deg_rank, toff.p, n_act, tot.p, al, s);
+  EH_CUDA(cudaMemcpyAsync(toff.p + n_act, tot.p, 8, cudaMemcpyDeviceToDevice, s));  // toff[n_act] = 2m
   DBuf<uint32_t> dplus(al, std::max<uint64_t>(1, n_act));
   EH_CUDA(cudaMemsetAsync(dplus.p, 0, std::max<uint64_t>(1, n_act) * 4, s));
   DBuf<uint32_t> tmp(al, std::max<uint64_t>(1, 2 * m));

@@ -283,11 +283,15 @@ __global__ void __launch_bounds__(kPBlock, radix_min_blocks<kPBlock, kRItems, (i
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRItems; ++r)
-    if ((rd[r] >> 16) < kInv) skeys[tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu)] = key[r];
+    if ((rd[r] >> 16) < kInv) {
+      EH_DASSERT(tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu) < (uint32_t)kRTile);
+      skeys[tdp[rd[r] >> 16] + wcnt[w][rd[r] >> 16] + (rd[r] & 0xFFFFu)] = key[r];
+    }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < tn; i += kPBlock) {
     const K k = skeys[i];
     const uint32_t dd = (uint32_t)(k >> shift) & kDM;
+    EH_DASSERT(goff[dd] + (i - tdp[dd]) < n);
     out[goff[dd] + (i - tdp[dd])] = k;
   }
 }

@@ -4,6 +4,8 @@
 #pragma once
 #include <cstdint>
 
+#include "check.cuh"
+
 namespace eh {
 
 // desc[v].w of every set of an EH_NO_ALGO graph (all uint): row dispatch never

@@ -77,6 +77,7 @@ __global__ void k_seg_regs(uint32_t* __restrict__ data, Seg sg, const uint32_t* 
   for (uint64_t t = warp; t < nids; t += nw) {
     const uint32_t v = ids[t];
     const uint32_t n = sg.len[v];
+    EH_DASSERT(n <= 32u * E);
     uint32_t* p = data + sg.off16[v] * 4;
     const uint32_t* q = sg.src(data, v);
     uint32_t x[E];
@@ -127,6 +128,7 @@ __device__ __forceinline__ void sort_group(uint32_t* __restrict__ data, const Se
     p = data + sg.off16[v] * 4;
     q = sg.src(data, v);
   }
+  EH_DASSERT(n <= (uint32_t)S);
   uint32_t x = ((uint32_t)sl < n) ? q[sl] : kPad;
   x = subwarp_bitonic<S>(x, lane);
   if ((uint32_t)sl < n) p[sl] = x;
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(kBigThreads) k_seg_big(uint32_t* __restrict__ 
     const uint32_t* q = sg.src(data, v);
     uint32_t N = 2048;
     while (N < n) N <<= 1;
+    EH_DASSERT(N <= (uint32_t)kBigMax);
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = (i < n) ? q[i] : kPad;
     __syncthreads();
     bitonic_smem<true>(s, N, threadIdx.x, blockDim.x);

@@ -19,6 +19,10 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libeh.so")
+# EH_LIB=checked loads the checked build (device-side bounds assertions, build.py
+# checked=True) -- used by the tests in place of compute-sanitizer
+if os.environ.get("EH_LIB") == "checked":
+    LIB_PATH = os.path.join(_PKG, "lib", "libeh_checked.so")
 
 EH_OK, EH_EINVAL, EH_ENOMEM, EH_ECUDA, EH_EUNSORTED = 0, -1, -2, -3, -4
 EH_COUNT_ERROR = 2**64 - 1

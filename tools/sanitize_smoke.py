@@ -1,7 +1,10 @@
-"""Small workload touching every kernel path, for compute-sanitizer (T7).
+"""Small workload touching every kernel path, for compute-sanitizer (T7) and for
+the bounds-checked build (EH_LIB=checked: lib/libeh_checked.so, csrc/check.cuh).
 
 Checks counts against closed forms / the oracle so a sanitizer run is also a
 parity run.  Usage: compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+or EH_LIB=checked python tools/sanitize_smoke.py [--configs] (--configs adds the
+C2-C4 loads and counts against the stored oracle values).
 """
 import os
 import sys
@@ -68,4 +71,16 @@ for t in range(200):
     a = a.astype(np.uint32)
     b = b.astype(np.uint32)
     assert np.array_equal(eh.intersect(a, b), np.intersect1d(a, b))
-print("sanitize smoke ok")
+if "--configs" in sys.argv:
+    import json
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                                       "golden", "configs_oracle.json")))["configs"]
+    for name in ("C2", "C3", "C4"):
+        cs, cd = synth.CONFIGS[name].generate()
+        with eh.Graph(cs, cd) as g:
+            assert g.count_triangles() == gold[name]["triangles"], name
+            assert g.count_4cliques() == gold[name]["four_cliques"], name
+            n = g.stats().n_active
+            assert g.count_4cliques_range(0, n // 2) + g.count_4cliques_range(n // 2, n) == gold[name]["four_cliques"]
+        print(name, "ok", flush=True)
+print("sanitize smoke ok", eh.eh.LIB_PATH)
