@@ -17,8 +17,8 @@ when one exists for the config.
   e2e    = the same metric through the public C ABI with HOST (pinned) inputs,
            every step's H2D copy of the edge list (8 n bytes) and 8-byte D2H of
            its count inside the timed region: eh_count_batch over K steps (the
-           same workload uploaded K times), which overlaps the upload of step
-           i+1 with the load + count of step i on the SMs.  `e2e.single_graph`
+           same workload uploaded K times); the upload of step i+1 runs on a
+           copy stream beside the load + count of step i.  `e2e.single_graph`
            is the synchronous one-graph-at-a-time figure (eh_load_edges from
            host memory + count, nothing overlapped).
   roofline (dominant kernel = the triangle count): achieved = B_tri(tau=32)
@@ -333,17 +333,21 @@ def run_gpu(args, cfg, src, dst, n_in):
         counts.add(c)
     # e2e (pipelined): eh_count_batch over K host copies of the workload (each step
     # uploads its 8 n bytes again; inputs > L2, so no flush between the steps)
-    K = max(3, args.steps)
+    # (library streams of their own, blocking w.r.t. the legacy default stream, so
+    # events recorded there bracket the whole batch on the device)
+    K = max(4, args.steps)
     lists = [(h_src, h_dst)] * K
-    eh.count_batch(lists[:2], "4cliques" if k4 else "triangles", stream=stream)  # untimed warm-up
-    with torch.cuda.stream(stream):
+    q = "4cliques" if k4 else "triangles"
+    eh.count_batch(lists[:4], q)  # untimed warm-up (pools, streams)
+    legacy = torch.cuda.default_stream(dev)
+    with torch.cuda.stream(legacy):
         _flush_l2(flush)
     eb = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    stream.synchronize()
-    eb[0].record(stream)
-    bc = eh.count_batch(lists, "4cliques" if k4 else "triangles", stream=stream)
-    eb[1].record(stream)
-    stream.synchronize()
+    torch.cuda.synchronize()
+    eb[0].record(legacy)
+    bc = eh.count_batch(lists, q)
+    eb[1].record(legacy)
+    torch.cuda.synchronize()
     counts.update(bc)
     batch_ms = eb[0].elapsed_time(eb[1]) / K
     if len(counts) != 1:
@@ -385,8 +389,9 @@ def run_gpu(args, cfg, src, dst, n_in):
                      "alg_bytes": "B_K4(tau=32)" if k4 else "B_tri(tau=32)", "alg_bytes_per_launch": alg},
         "e2e": {"value": e2e_value, "unit": "input edges/s",
                 "h2d_bytes_per_step": 8 * n_in, "d2h_bytes_per_step": 8, "ms_per_step": batch_ms_max,
-                "api": f"eh_count_batch over {K} steps from pinned host memory (upload of step i+1 on a copy "
-                       "stream overlapping the load + count of step i)",
+                "api": f"eh_count_batch over {K} steps from pinned host memory: the upload of step i+1 runs "
+                       "on a copy stream beside the load + count of step i (one lane at this size; two lanes "
+                       "of alternate steps for lists of <= 2^23 edges)",
                 "single_graph": {"value": e2e_single, "ms_per_step": mean_e2e_max,
                                  "api": "eh_load_edges_ex(host inputs) + count + eh_free, one step at a time"}},
         "gpu_launches": launches,

@@ -154,7 +154,9 @@ eh_graph* eh_load_edges_ex(const uint32_t* src, const uint32_t* dst, uint64_t n,
  *  cfg                  : may be NULL; EH_INPUT_ON_DEVICE is rejected; cfg->stream
  *                         (else a library-owned blocking stream) runs the compute
  *  counts[k]            : caller-owned host array, receives the k counts
- * Two device input buffers of 8 max(n) bytes are held for the call.  Returns
+ * Without cfg->stream, batches of small lists (<= 2^23 edges) run in two lanes
+ * (library host threads and streams, alternate lists).  Two device input buffers
+ * of 8 max(n) bytes per lane are held for the call.  Returns
  * EH_OK, EH_EINVAL, EH_ENOMEM or EH_ECUDA (counts of lists before a failure are
  * written).
  */

@@ -6,6 +6,8 @@
 #include "eh_internal.cuh"
 
 #include <cstring>
+#include <exception>
+#include <thread>
 
 namespace eh {
 std::atomic<unsigned long long> g_launches{0};
@@ -165,6 +167,88 @@ eh_graph* load_impl(const uint32_t* src, const uint32_t* dst, uint64_t n, const 
 }
 
 
+
+// One lane of eh_count_batch: lists first, first + step, ... in order on one compute
+// stream (the caller's, else a blocking library stream), uploads on a non-blocking
+// copy stream into two device input buffers (ping-pong): the upload of the lane's
+// next list overlaps the load + count of the current one.
+void batch_lane(const uint32_t* const* src, const uint32_t* const* dst, const uint64_t* n, uint64_t k,
+                uint64_t first, uint64_t step, uint32_t query, const eh_config& c, uint64_t* counts) {
+  uint64_t nmax = 0;
+  for (uint64_t i = first; i < k; i += step) nmax = std::max(nmax, n[i]);
+  cudaStream_t cs = (cudaStream_t)c.stream, up = nullptr;
+  bool own_cs = false;
+  cudaEvent_t landed[2] = {nullptr, nullptr}, read[2] = {nullptr, nullptr};
+  eh::Allocator al;
+  al.hook_alloc = c.dev_alloc;
+  al.hook_free = c.dev_free;
+  al.ctx = c.alloc_ctx;
+  void* buf[2] = {nullptr, nullptr};
+  auto cleanup = [&]() {
+    if (cs) cudaStreamSynchronize(cs);
+    if (up) cudaStreamSynchronize(up);
+    for (int b = 0; b < 2; ++b) {
+      if (buf[b]) al.release(buf[b]);
+      if (landed[b]) cudaEventDestroy(landed[b]);
+      if (read[b]) cudaEventDestroy(read[b]);
+    }
+    if (cs) cudaStreamSynchronize(cs);
+    if (up) cudaStreamDestroy(up);
+    if (own_cs && cs) cudaStreamDestroy(cs);
+  };
+  try {
+    if (!cs) {
+      EH_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamDefault));
+      own_cs = true;
+    }
+    EH_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    al.stream = cs;
+    for (int b = 0; b < 2; ++b) {
+      EH_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
+      EH_CUDA(cudaEventCreateWithFlags(&read[b], cudaEventDisableTiming));
+      buf[b] = al.alloc(std::max<uint64_t>(1, 2 * nmax) * 4);
+    }
+    EH_CUDA(cudaStreamSynchronize(cs));  // the buffers exist before the copy stream writes them
+    auto upload = [&](uint64_t j) {  // j-th list of this lane
+      const uint64_t i = first + j * step;
+      const int b = (int)(j & 1);
+      uint32_t* d = (uint32_t*)buf[b];
+      if (j >= 2) EH_CUDA(cudaStreamWaitEvent(up, read[b], 0));  // the lane's list j-2 has been read
+      if (n[i]) {
+        EH_CUDA(cudaMemcpyAsync(d, src[i], n[i] * 4, cudaMemcpyHostToDevice, up));
+        EH_CUDA(cudaMemcpyAsync(d + n[i], dst[i], n[i] * 4, cudaMemcpyHostToDevice, up));
+      }
+      EH_CUDA(cudaEventRecord(landed[b], up));
+    };
+    eh_config gc = c;
+    gc.flags |= EH_INPUT_ON_DEVICE;
+    gc.flags &= ~(uint32_t)EH_SET_DEVICE;
+    gc.stream = cs;
+    const uint64_t nl = (k - first + step - 1) / step;
+    upload(0);
+    for (uint64_t j = 0; j < nl; ++j) {
+      if (j + 1 < nl) upload(j + 1);  // overlaps the load and count of list j
+      const uint64_t i = first + j * step;
+      const int b = (int)(j & 1);
+      EH_CUDA(cudaStreamWaitEvent(cs, landed[b], 0));
+      const uint32_t* d = (const uint32_t*)buf[b];
+      eh_graph* g = load_impl(d, d + n[i], n[i], &gc);  // synchronous on cs: inputs read on return
+      EH_CUDA(cudaEventRecord(read[b], cs));
+      try {
+        counts[i] = query == EH_QUERY_4CLIQUES ? eh::count_4cliques(g) : eh::count_triangles(g);
+      } catch (...) {
+        destroy(g);
+        throw;
+      }
+      destroy(g);
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
 }  // namespace
 
 extern "C" {
@@ -188,11 +272,8 @@ int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const
     if (cfg) c = *cfg;
     if (c.flags & EH_INPUT_ON_DEVICE) eh::fail(EH_EINVAL, "eh_count_batch: inputs are host memory");
     if (k == 0) return EH_OK;
-    uint64_t nmax = 0;
-    for (uint64_t i = 0; i < k; ++i) {
+    for (uint64_t i = 0; i < k; ++i)
       if (n[i] && (!src[i] || !dst[i])) eh::fail(EH_EINVAL, "eh_count_batch: NULL list %llu", (unsigned long long)i);
-      nmax = std::max(nmax, n[i]);
-    }
     int dev = 0, ndev = 0;
     EH_CUDA(cudaGetDeviceCount(&ndev));
     if (ndev <= 0) eh::fail(EH_ECUDA, "no CUDA device");
@@ -202,76 +283,32 @@ int eh_count_batch(const uint32_t* const* src, const uint32_t* const* dst, const
       dev = c.device;
     }
     DeviceGuard guard(dev);
-    // compute stream: the caller's, else a blocking library stream; uploads on a
-    // non-blocking copy stream, two device input buffers (ping-pong)
-    cudaStream_t cs = (cudaStream_t)c.stream, up = nullptr;
-    bool own_cs = false;
-    cudaEvent_t landed[2] = {nullptr, nullptr}, read[2] = {nullptr, nullptr};
-    eh::Allocator al;
-    al.hook_alloc = c.dev_alloc;
-    al.hook_free = c.dev_free;
-    al.ctx = c.alloc_ctx;
-    void* buf[2] = {nullptr, nullptr};
-    auto cleanup = [&]() {
-      if (cs) cudaStreamSynchronize(cs);
-      if (up) cudaStreamSynchronize(up);
-      for (int b = 0; b < 2; ++b) {
-        if (buf[b]) al.release(buf[b]);
-        if (landed[b]) cudaEventDestroy(landed[b]);
-        if (read[b]) cudaEventDestroy(read[b]);
+    // lanes: with the caller's stream one lane runs every list on it; otherwise small
+    // lists (<= 2^23 input edges) take two lanes (host threads with streams of their
+    // own, alternate lists), so one list's ingest and count kernels fill the gaps of
+    // the other's; large lists keep one lane -- two graphs in flight evict each other's
+    // L2-resident hub lists (measured, ms per list: C2 1.48 -> 1.37 with two lanes,
+    // C4 K4 10.69 -> 10.76, C3 16.8 -> 18.2).  Test hook EH_TEST_BATCH_LANES=1|2.
+    uint64_t nmax = 0;
+    for (uint64_t i = 0; i < k; ++i) nmax = std::max(nmax, n[i]);
+    int lanes = (c.stream || nmax > (1ull << 23)) ? 1 : 2;
+    if (const char* e = getenv("EH_TEST_BATCH_LANES")) lanes = std::max(1, std::min(2, atoi(e)));
+    if ((uint64_t)lanes > k) lanes = (int)k;
+    std::exception_ptr err[2];
+    auto run = [&](int lane) {
+      try {
+        EH_CUDA(cudaSetDevice(dev));
+        batch_lane(src, dst, n, k, (uint64_t)lane, (uint64_t)lanes, query, c, counts);
+      } catch (...) {
+        err[lane] = std::current_exception();
       }
-      if (cs) cudaStreamSynchronize(cs);
-      if (up) cudaStreamDestroy(up);
-      if (own_cs && cs) cudaStreamDestroy(cs);
     };
-    try {
-      if (!cs) {
-        EH_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamDefault));
-        own_cs = true;
-      }
-      EH_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-      al.stream = cs;
-      for (int b = 0; b < 2; ++b) {
-        EH_CUDA(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming));
-        EH_CUDA(cudaEventCreateWithFlags(&read[b], cudaEventDisableTiming));
-        buf[b] = al.alloc(std::max<uint64_t>(1, 2 * nmax) * 4);
-      }
-      EH_CUDA(cudaStreamSynchronize(cs));  // the buffers exist before the copy stream writes them
-      auto upload = [&](uint64_t i) {
-        const int b = (int)(i & 1);
-        uint32_t* d = (uint32_t*)buf[b];
-        if (i >= 2) EH_CUDA(cudaStreamWaitEvent(up, read[b], 0));  // list i-2 has been read
-        if (n[i]) {
-          EH_CUDA(cudaMemcpyAsync(d, src[i], n[i] * 4, cudaMemcpyHostToDevice, up));
-          EH_CUDA(cudaMemcpyAsync(d + n[i], dst[i], n[i] * 4, cudaMemcpyHostToDevice, up));
-        }
-        EH_CUDA(cudaEventRecord(landed[b], up));
-      };
-      eh_config gc = c;
-      gc.flags |= EH_INPUT_ON_DEVICE;
-      gc.flags &= ~(uint32_t)EH_SET_DEVICE;
-      gc.stream = cs;
-      upload(0);
-      for (uint64_t i = 0; i < k; ++i) {
-        if (i + 1 < k) upload(i + 1);  // overlaps the load and count of list i
-        const int b = (int)(i & 1);
-        EH_CUDA(cudaStreamWaitEvent(cs, landed[b], 0));
-        const uint32_t* d = (const uint32_t*)buf[b];
-        eh_graph* g = load_impl(d, d + n[i], n[i], &gc);  // synchronous on cs: inputs read on return
-        EH_CUDA(cudaEventRecord(read[b], cs));
-        try {
-          counts[i] = query == EH_QUERY_4CLIQUES ? eh::count_4cliques(g) : eh::count_triangles(g);
-        } catch (...) {
-          destroy(g);
-          throw;
-        }
-        destroy(g);
-      }
-    } catch (...) {
-      cleanup();
-      throw;
-    }
-    cleanup();
+    std::thread other;
+    if (lanes == 2) other = std::thread(run, 1);
+    run(0);
+    if (other.joinable()) other.join();
+    for (int l = 0; l < lanes; ++l)
+      if (err[l]) std::rethrow_exception(err[l]);
     return EH_OK;
   });
 }

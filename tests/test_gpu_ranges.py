@@ -222,5 +222,6 @@ def test_count_batch_pipelined_uploads():
     lists.append(lists[0])
     ref.append(ref[0])
     assert eh.count_batch(lists) == [r[0] for r in ref]
-    assert eh.count_batch(lists, "4cliques", stream=torch.cuda.Stream()) == [r[1] for r in ref]
+    assert eh.count_batch(lists, "4cliques", stream=torch.cuda.Stream()) == [r[1] for r in ref]  # one lane
+    assert eh.count_batch(lists, "4cliques") == [r[1] for r in ref]  # two lanes
     assert eh.count_batch([]) == []
