@@ -853,8 +853,10 @@ uint64_t count_impl(eh_graph* g) {
     // (measured C3 8.59 -> 8.38 ms, C4 1.458 -> 1.419, C2 0.316 -> 0.313)
     const uint32_t* w0 = g->work + nt;
     const uint64_t n0 = nsmall - nt;
+    // rows on 4-lane groups below 2^20 active ids (8 rows in flight per warp; measured
+    // C4 1.264 -> 1.251, C2 0.270 -> 0.268 ms; above, with the pivot searches, C3 7.87 -> 8.07)
     if (!wide && g->class0_max <= 64 && big) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16, true>(g, n0, w0, 1u, ss);
-    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, kG, 16>(g, n0, w0, 1u, ss);
+    else if (!wide && g->class0_max <= 64) launch_warp<kUnpruned, kBlock, 64, 6, 4, 16>(g, n0, w0, 1u, ss);
     else if (!wide) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16>(g, n0, w0, 1u, ss);
     else if (kUnpruned && g->n_act <= kWideIds) launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 16, true>(g, n0, w0, 1u, ss);
     else if (!kUnpruned && !kBlock && g->class0_max <= 64) {  // wide: class 0 with 64-entry staging, min 6 CTAs/SM
