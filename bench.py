@@ -170,13 +170,14 @@ def aggregate(dist, ws: int, n_in_per_rank: int, local_ms: float, device="cpu"):
     return ws * n_in_per_rank / (mx / 1e3), mx
 
 
-def _traffic():
+def _traffic(cfg_name: str, k4: bool):
     """DRAM bytes (read + write) per launch of the count kernels, from the
-    committed `ncu --set full` capture (profiles/traffic.json), else None."""
+    committed `ncu --set full` capture (profiles/traffic.json) of this config and
+    query, else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("tri_C3_bytes_per_launch")
+        return d.get(f"{'k4' if k4 else 'tri'}_{cfg_name}_bytes_per_launch")
     return None
 
 
@@ -384,7 +385,7 @@ def run_gpu(args, cfg, src, dst, n_in):
         "count_edges_per_s": n_in / (mean_count / 1e3),
         ("four_cliques_per_s" if k4 else "triangles_per_s"): T / (mean_count / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None if k4 else _traffic(), "peak_kind": peak_kind,
+                     "traffic": _traffic(cfg.name, k4), "peak_kind": peak_kind,
                      "kernel": "k_k4_* (eh_count_4cliques)" if k4 else "k_tri_* (eh_count_triangles)",
                      "alg_bytes": "B_K4(tau=32)" if k4 else "B_tri(tau=32)", "alg_bytes_per_launch": alg},
         "e2e": {"value": e2e_value, "unit": "input edges/s",
