@@ -839,7 +839,7 @@ uint64_t count_impl(eh_graph* g) {
   // The thread- and warp-class kernels run on a side stream beside the CTA-class
   // kernel (they share only the count, an atomic), so the tail of one overlaps the
   // other; test hook EH_TEST_TRI_SERIAL keeps one stream.
-  const cudaStream_t ss = getenv("EH_TEST_TRI_SERIAL") == nullptr ? fork_side(g, 0) : s;
+  const cudaStream_t ss = (nlarge && nsmall && getenv("EH_TEST_TRI_SERIAL") == nullptr) ? fork_side(g, 0) : s;
   // a7 thread class (the head of class 0; pruned set-level nest only)
   const uint64_t nt = (!kUnpruned && !kBlock) ? g->n_thread : 0;
   launch_thread(g, nt, ss);

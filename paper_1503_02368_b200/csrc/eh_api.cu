@@ -11,6 +11,13 @@
 
 namespace eh {
 std::atomic<unsigned long long> g_launches{0};
+
+SideStreams& side_streams(int device) {
+  constexpr int kMaxDev = 64;
+  if (device < 0 || device >= kMaxDev) fail(EH_EINVAL, "device ordinal %d out of range", device);
+  thread_local SideStreams per_dev[kMaxDev];  // process lifetime of the thread; never destroyed
+  return per_dev[device];
+}
 }
 
 namespace {
@@ -45,16 +52,6 @@ R guarded(R on_error, F&& f) {
   return on_error;
 }
 
-void release_sides(eh_graph* g) {
-  for (int k = 0; k < eh_graph::kSides; ++k)
-    if (g->side[k]) {
-      cudaStreamSynchronize(g->side[k]);
-      cudaStreamDestroy(g->side[k]);
-      cudaEventDestroy(g->ev_join[k]);
-    }
-  if (g->ev_fork) cudaEventDestroy(g->ev_fork);
-}
-
 template <class F>
 int guarded_status(F&& f) {
   const int r = guarded<int>(INT32_MIN, std::forward<F>(f));
@@ -69,11 +66,9 @@ void destroy(eh_graph* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->sym) {
     eh_graph* h = g->sym;
-    release_sides(h);
     for (void* p : h->owned) h->alloc.release(p);
     delete h;
   }
-  release_sides(g);
   for (void* p : g->owned) g->alloc.release(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);

@@ -245,10 +245,7 @@ struct eh_graph {
   unsigned long long* d_counter = nullptr;  // 8 x u64: count, work cursors, y-major queue size
   unsigned long long h_counter[2] = {0, 0};  // host mirror (8-byte D2H per count)
   eh_graph* sym = nullptr;  // NEXT-2: symmetric (unpruned) trie, built on first use (sym.cu)
-  // side streams + fork / join events of the count kernels (created on first use)
-  static constexpr int kSides = 3;
-  cudaStream_t side[kSides] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join[kSides] = {};
+
 
   std::vector<void*> owned;  // every device allocation above
   uint64_t device_bytes = 0;
@@ -287,22 +284,32 @@ class WorkRange {
   uint64_t saved_n_[3], saved_nt_;
   DBuf<uint32_t> work_, lpt_;
 };
-// Fork: side stream k of the handle (non-blocking, created on first use) waits for
-// the work queued so far on the handle's stream.  Join: the handle's stream waits
-// for everything queued on side stream k.
+// Side streams of the count kernels: per host thread and device, created once
+// (non-blocking) with their fork / join events, so a count on a fresh handle pays
+// no stream creation.  Fork: side stream k waits for the work queued so far on the
+// handle's stream.  Join: the handle's stream waits for everything queued on side
+// stream k.  (Every count call joins before it returns.)
+struct SideStreams {
+  static constexpr int kSides = 3;
+  cudaStream_t s[kSides] = {};
+  cudaEvent_t fork = nullptr, join[kSides] = {};
+};
+SideStreams& side_streams(int device);  // eh_api.cu
 inline cudaStream_t fork_side(eh_graph* g, int k) {
-  if (!g->ev_fork) EH_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-  if (!g->side[k]) {
-    EH_CUDA(cudaStreamCreateWithFlags(&g->side[k], cudaStreamNonBlocking));
-    EH_CUDA(cudaEventCreateWithFlags(&g->ev_join[k], cudaEventDisableTiming));
+  SideStreams& ss = side_streams(g->device);
+  if (!ss.fork) EH_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+  if (!ss.s[k]) {
+    EH_CUDA(cudaStreamCreateWithFlags(&ss.s[k], cudaStreamNonBlocking));
+    EH_CUDA(cudaEventCreateWithFlags(&ss.join[k], cudaEventDisableTiming));
   }
-  EH_CUDA(cudaEventRecord(g->ev_fork, g->stream));
-  EH_CUDA(cudaStreamWaitEvent(g->side[k], g->ev_fork, 0));
-  return g->side[k];
+  EH_CUDA(cudaEventRecord(ss.fork, g->stream));
+  EH_CUDA(cudaStreamWaitEvent(ss.s[k], ss.fork, 0));
+  return ss.s[k];
 }
 inline void join_side(eh_graph* g, int k) {
-  EH_CUDA(cudaEventRecord(g->ev_join[k], g->side[k]));
-  EH_CUDA(cudaStreamWaitEvent(g->stream, g->ev_join[k], 0));
+  SideStreams& ss = side_streams(g->device);
+  EH_CUDA(cudaEventRecord(ss.join[k], ss.s[k]));
+  EH_CUDA(cudaStreamWaitEvent(g->stream, ss.join[k], 0));
 }
 // count_tri.cu / count_k4.cu
 uint64_t count_triangles(eh_graph* g);
