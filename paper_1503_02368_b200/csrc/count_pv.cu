@@ -416,6 +416,9 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
   cudaStream_t s = g->stream;
   const uint64_t nsmall = g->n_work[0];  // class 0 -> warp kernel; classes 1-2 -> CTA kernel
   const uint64_t nlarge = g->n_work[1] + g->n_work[2];
+  const uint32_t* wl = nlarge ? work_lpt(g) + nsmall : nullptr;
+  // the warp-class kernel on a side stream beside the CTA-class kernel (count_tri.cu)
+  const cudaStream_t ss = (nlarge && nsmall && getenv("EH_TEST_TRI_SERIAL") == nullptr) ? fork_side(g, 0) : s;
   if (nlarge) {
     // N+(x) staged up to max |N+(x)| rounded up to 256 (smaller CTAs than a power of
     // two >= 2048: C3 t(v) 13.89 -> 13.80 ms, C4 2.34 -> 2.27 ms)
@@ -428,8 +431,7 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
     int per_sm = 0;
     EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-    kc<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, work_lpt(g) + nsmall, nlarge, d_t, sf16,
-                                           g->d_counter, xc);
+    kc<<<grid, kCtaWarps * 32, smem, s>>>(g->desc, g->col, g->bs, wl, nlarge, d_t, sf16, g->d_counter, xc);
     EH_LAUNCH("k_pv_cta");
   }
   if (nsmall) {
@@ -437,9 +439,10 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
     const size_t smem = sizeof(PvWarpSmem) * kWarps;
     auto kw = k_pv_warp<kPiv>;
     EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kw<<<grid, kWarps * 32, smem, s>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
+    kw<<<grid, kWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
     EH_LAUNCH("k_pv_warp");
   }
+  if (ss != s) join_side(g, 0);
 }
 
 }  // namespace
