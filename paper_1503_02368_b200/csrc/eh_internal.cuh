@@ -293,6 +293,16 @@ struct SideStreams {
   static constexpr int kSides = 3;
   cudaStream_t s[kSides] = {};
   cudaEvent_t fork = nullptr, join[kSides] = {};
+  SideStreams() = default;
+  SideStreams(const SideStreams&) = delete;
+  SideStreams& operator=(const SideStreams&) = delete;
+  ~SideStreams() {  // at thread exit (e.g. an eh_count_batch lane); errors after CUDA teardown are ignored
+    for (int k = 0; k < kSides; ++k) {
+      if (s[k]) cudaStreamDestroy(s[k]);
+      if (join[k]) cudaEventDestroy(join[k]);
+    }
+    if (fork) cudaEventDestroy(fork);
+  }
 };
 SideStreams& side_streams(int device);  // eh_api.cu
 inline cudaStream_t fork_side(eh_graph* g, int k) {
