@@ -18,10 +18,11 @@
 // Then the innermost loop is a bit-parallel AND:
 //     K(x) = sum over set bits (i, j) of popcount(L_i & L_j restricted to > j),
 // i.e. |P cap N+(z)| with P = N+(x) cap N+(y), y = x_i, z = x_j, counted 32 w
-// at a time.  |N+(x)| <= 128: one warp per x (rows on 8-lane groups, then 4-lane
-// groups over the <= 4 words of a row); 128 < |N+(x)| <= 1024: one CTA per x
-// (L up to 192 KB of shared memory); larger x (rare when pruned; the hubs of the
-// symmetric data): one CTA per row (k_k4_big).  COUNT(*) accumulates per lane in u64 (K4 > 2^32 on C4).
+// at a time.  |N+(x)| <= 128: one warp per x (rows on 8-lane groups, then 2- or
+// 4-lane groups over the <= 2 / 4 words of a row; a half-size instance for
+// |N+(x)| <= 64); 128 < |N+(x)| <= 1024: one CTA per x (three shapes of 8 / 32 / 32
+// warps, L up to 135 KB of shared memory); larger x (rare when pruned; the hubs of
+// the symmetric data): one CTA per row (k_k4_big).  COUNT(*) accumulates per lane in u64 (K4 > 2^32 on C4).
 #include "eh_internal.cuh"
 #include "primitives.cuh"
 #include "rows.cuh"
@@ -33,11 +34,9 @@ namespace {
 
 constexpr int kG = 8;                 // lanes per row group (row fill)
 constexpr int kWMaxD = 128;           // warp kernel: d <= 128 -> rows of <= 4 words
-constexpr int kWW = 4;                // row stride (words) in the warp kernel
-constexpr int kWHash = 512;           // hash slots >= 4d
 constexpr int kWWarps = 8;
 constexpr int kCMaxD = 1024;          // CTA kernels: d <= 1024 -> rows of <= 32 words; three shapes
-                                      // (d <= 256: 4 warps; <= 512: 8 warps, ~57 KB; larger: 16 warps, 192 KB)
+                                      // (d <= 256: 8 warps, ~25 KB; <= 512: 32 warps, ~82 KB; larger: 32 warps, 224 KB)
 constexpr uint32_t kEmptyK = 0xFFFFFFFFu;
 
 enum K4Kind : uint8_t { kKSkip = 0, kKProbe = 1, kKStream = 2, kKSearch = 3 };
@@ -117,41 +116,49 @@ __device__ __forceinline__ void fill_row(uint8_t kd, const uint32_t* __restrict_
 }
 
 // ------------------------------------------------------------ warp kernel --
+// per-warp shared memory of the warp kernel for |N+(x)| <= kMD: rows of kMD / 32
+// words, a local hash of 4 kMD slots
+template <int kMD>
 struct __align__(16) K4WarpSmem {
-  uint32_t xs[kWMaxD];
-  uint32_t hkeys[kWHash];
-  uint32_t L[kWMaxD * kWW];
-  YInfo yi[kWMaxD];
-  uint16_t hidx[kWHash];
-  uint8_t kind[kWMaxD];
-  uint8_t ord[kWMaxD];
+  static constexpr int kW = kMD / 32;
+  uint32_t xs[kMD];
+  uint32_t hkeys[4 * kMD];
+  uint32_t L[kMD * kW];
+  YInfo yi[kMD];
+  uint16_t hidx[4 * kMD];
+  uint8_t kind[kMD];
+  uint8_t ord[kMD];
 };
 
-template <bool kU>
+// kMD = 64 (class 0) or kWMaxD = 128; the smaller instance has half the shared
+// memory per warp, so about twice as many warps per SM
+template <bool kU, int kMD = kWMaxD>
 __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restrict__ desc,
                                                           const uint32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ bs,
                                                           const uint32_t* __restrict__ work, uint64_t nwork,
-                                                          unsigned long long* __restrict__ ctr, uint32_t sf16) {
+                                                          unsigned long long* __restrict__ ctr, uint32_t sf16,
+                                                          uint32_t cslot) {
+  constexpr uint32_t kWWd = K4WarpSmem<kMD>::kW;
   extern __shared__ __align__(16) uint32_t dsm_k4w[];
-  K4WarpSmem& sm = reinterpret_cast<K4WarpSmem*>(dsm_k4w)[threadIdx.x >> 5];
+  K4WarpSmem<kMD>& sm = reinterpret_cast<K4WarpSmem<kMD>*>(dsm_k4w)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   unsigned long long cnt = 0;
   for (;;) {
     unsigned long long wi = 0;
-    if (lane == 0) wi = atomicAdd(&ctr[1], 1ull);
+    if (lane == 0) wi = atomicAdd(&ctr[cslot], 1ull);
     wi = __shfl_sync(kFull, wi, 0);
     if (wi >= nwork) break;
     const uint32_t x = __ldg(work + wi);
     const uint4 dx = __ldg(desc + x);
-    const uint32_t d = dx.y;  // 2 <= d <= kWMaxD
-    EH_DASSERT(d >= 2 && d <= (uint32_t)kWMaxD);
+    const uint32_t d = dx.y;  // 2 <= d <= kMD
+    EH_DASSERT(d >= 2 && d <= (uint32_t)kMD);
     if (d < 3) continue;
     const uint32_t* xg = col + (uint64_t)dx.x * 4;
     for (uint32_t k = lane; k < (d + 3) / 4; k += 32)
       reinterpret_cast<uint4*>(sm.xs)[k] = __ldg(reinterpret_cast<const uint4*>(xg) + k);
-    for (uint32_t k = lane; k < d * kWW; k += 32) sm.L[k] = 0u;
+    for (uint32_t k = lane; k < d * kWWd; k += 32) sm.L[k] = 0u;
     __syncwarp();
     const LocalHash H = build_local_hash<false>(sm.hkeys, sm.hidx, sm.xs, d, lane, 32);
     const uint32_t nrows = kU ? d : d - 1;
@@ -176,23 +183,23 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
     __syncwarp();
     for (uint32_t r = lane / kG; r < nr; r += 32 / kG) {
       const uint32_t i = sm.ord[r];
-      fill_row<kU>(sm.kind[i], col, bs, sm.yi[i], sm.xs, d, i, H, sm.L + i * kWW, lane % kG);
+      fill_row<kU>(sm.kind[i], col, bs, sm.yi[i], sm.xs, d, i, H, sm.L + i * kWWd, lane % kG);
     }
     __syncwarp();
-    // bit-parallel innermost loop: 4-lane groups, lane q holds word q of row i
-    const uint32_t W = (d + 31) >> 5, q = lane & 3;
-    for (uint32_t i0 = 0; i0 < d; i0 += 8) {
-      const uint32_t i = i0 + (lane >> 2);
-      const uint32_t li = (i < d && q < W) ? sm.L[i * kWW + q] : 0u;
+    // bit-parallel innermost loop: kWWd-lane groups, lane q holds word q of row i
+    const uint32_t W = (d + 31) >> 5, q = lane & (kWWd - 1);
+    for (uint32_t i0 = 0; i0 < d; i0 += 32 / kWWd) {
+      const uint32_t i = i0 + lane / kWWd;
+      const uint32_t li = (i < d && q < W) ? sm.L[i * kWWd + q] : 0u;
       for (uint32_t kk = 0; kk < W; ++kk) {
-        uint32_t wb = __shfl_sync(kFull, li, (lane & ~3) + kk);
+        uint32_t wb = __shfl_sync(kFull, li, (lane & ~(kWWd - 1)) + kk);
         while (wb) {
           const uint32_t b = __ffs(wb) - 1;
           wb &= wb - 1;
           const uint32_t j = kk * 32 + b;
           if (kU ? q < W : (q >= kk && q < W)) {  // unpruned: all w, else w after z
             const uint32_t m = (kU || q != kk) ? 0xFFFFFFFFu : ~((2u << b) - 1u);
-            cnt += __popc(li & sm.L[j * kWW + q] & m);
+            cnt += __popc(li & sm.L[j * kWWd + q] & m);
           }
         }
       }
@@ -470,6 +477,19 @@ __global__ void __launch_bounds__(kBigThreads) k_k4_big(const uint4* __restrict_
   if (lane == 0 && cnt) atomicAdd(&ctr[0], cnt);
 }
 
+template <bool kU, int kMaxD, int kCWarps>
+void launch_k4_cta(eh_graph* g, const uint32_t* wl, uint64_t nlarge, uint32_t dlo, uint32_t cslot, uint32_t sf16,
+                   cudaStream_t st) {
+  constexpr size_t smem = k4_cta_smem<kMaxD, kCWarps>();
+  auto k = k_k4_cta<kU, kMaxD, kCWarps>;
+  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCWarps * 32, smem));
+  const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
+  k<<<grid, kCWarps * 32, smem, st>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, dlo, cslot, sf16);
+  EH_LAUNCH("k_k4_cta");
+}
+
 template <bool kU>
 uint64_t k4_impl(eh_graph* g) {
   cudaStream_t s = g->stream;
@@ -488,41 +508,49 @@ uint64_t k4_impl(eh_graph* g) {
   const cudaStream_t s1 = (shapes && nlarge) ? fork_side(g, 1) : s;
   const cudaStream_t s2 = (shapes && nlarge && g->max_dplus > 512) ? fork_side(g, 2) : s;
   if (nsmall) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
-    const size_t smem = sizeof(K4WarpSmem) * kWWarps;
-    EH_CUDA(cudaFuncSetAttribute(k_k4_warp<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_k4_warp<kU><<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, nsmall, g->d_counter, sf16);
-    EH_LAUNCH("k_k4_warp");
+    // class 0 (|N+(x)| <= 64) on the half-size instance when it holds all of it, the
+    // rest (<= 128) after it on the same stream (its own work cursor, slot 6)
+    const uint64_t n64 = (g->class0_max <= 64 && getenv("EH_TEST_K4_W128") == nullptr) ? g->n_work[0] : 0;
+    if (n64) {
+      auto kw = k_k4_warp<kU, 64>;
+      const size_t smem = sizeof(K4WarpSmem<64>) * kWWarps;
+      EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kw, kWWarps * 32, smem));
+      const unsigned grid = (unsigned)std::min<uint64_t>((n64 + kWWarps - 1) / kWWarps, (uint64_t)kSMs * std::max(1, per_sm));
+      kw<<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, n64, g->d_counter, sf16, 6u);
+      EH_LAUNCH("k_k4_warp");
+    }
+    if (nsmall > n64) {
+      auto kw = k_k4_warp<kU, kWMaxD>;
+      const size_t smem = sizeof(K4WarpSmem<kWMaxD>) * kWWarps;
+      EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const unsigned grid = (unsigned)std::min<uint64_t>((nsmall - n64 + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
+      kw<<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work + n64, nsmall - n64, g->d_counter, sf16,
+                                            1u);
+      EH_LAUNCH("k_k4_warp");
+    }
   }
   if (nlarge) {
-    // d <= 256: 4-warp CTAs (~20 KB); d <= 512: 8-warp CTAs (~57 KB); 512 < d <= 1024: 16 warps, ~190 KB
-    {
-      constexpr size_t sm0 = k4_cta_smem<256, 4>();
-      auto k0 = k_k4_cta<kU, 256, 4>;
-      EH_CUDA(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
-      int per_sm = 0;
-      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k0, 4 * 32, sm0));
-      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k0<<<grid, 4 * 32, sm0, s>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 0u, 5u, sf16);
-      EH_LAUNCH("k_k4_cta");
-    }
-    {
-      constexpr size_t sm1 = k4_cta_smem<512, 8>();
-      auto k1 = k_k4_cta<kU, 512, 8>;
-      EH_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
-      int per_sm = 0;
-      EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 8 * 32, sm1));
-      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
-      k1<<<grid, 8 * 32, sm1, s1>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 256u, 2u, sf16);
-      EH_LAUNCH("k_k4_cta");
-    }
+    // d <= 256: 8-warp CTAs (~25 KB); d <= 512: 32-warp CTAs (~82 KB); d <= 1024: 32 warps
+    // (224 KB, one CTA per SM): more warps per x than round 1's 4 / 8 / 16 -- the fills
+    // and the bit-parallel loop of one x are latency-bound, so more of them in flight
+    // (measured: C4 K4 6.78 -> 6.20 (256: 8, 512: 16) -> 5.96 ms (512, 1024: 32), C3 43.4
+    // -> 39.7 -> 34.9; 256-shape with 16 warps slower).  Test hooks EH_TEST_K4_W256 /
+    // _W512 / _W1024 select other warp counts.
+    const char* w256 = getenv("EH_TEST_K4_W256");
+    const char* w512 = getenv("EH_TEST_K4_W512");
+    const int nw256 = w256 ? atoi(w256) : 8, nw512 = w512 ? atoi(w512) : 32;
+    if (nw256 == 4) launch_k4_cta<kU, 256, 4>(g, wl, nlarge, 0u, 5u, sf16, s);
+    else if (nw256 == 16) launch_k4_cta<kU, 256, 16>(g, wl, nlarge, 0u, 5u, sf16, s);
+    else launch_k4_cta<kU, 256, 8>(g, wl, nlarge, 0u, 5u, sf16, s);
+    if (nw512 == 8) launch_k4_cta<kU, 512, 8>(g, wl, nlarge, 256u, 2u, sf16, s1);
+    else if (nw512 == 16) launch_k4_cta<kU, 512, 16>(g, wl, nlarge, 256u, 2u, sf16, s1);
+    else launch_k4_cta<kU, 512, 32>(g, wl, nlarge, 256u, 2u, sf16, s1);
     if (g->max_dplus > 512) {
-      constexpr size_t sm2 = k4_cta_smem<kCMaxD, 16>();
-      auto k2 = k_k4_cta<kU, kCMaxD, 16>;
-      EH_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-      const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs);
-      k2<<<grid, 16 * 32, sm2, s2>>>(g->desc, g->col, g->bs, wl, nlarge, g->d_counter, 512u, 4u, sf16);
-      EH_LAUNCH("k_k4_cta");
+      const char* w1024 = getenv("EH_TEST_K4_W1024");
+      if (w1024 && atoi(w1024) == 16) launch_k4_cta<kU, kCMaxD, 16>(g, wl, nlarge, 512u, 4u, sf16, s2);
+      else launch_k4_cta<kU, kCMaxD, 32>(g, wl, nlarge, 512u, 4u, sf16, s2);
     }
     if (g->max_dplus > (uint64_t)kCMaxD) {
       DBuf<uint32_t> bx(g->alloc, nlarge), brows(g->alloc, nlarge);
