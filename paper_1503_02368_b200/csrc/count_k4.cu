@@ -521,7 +521,13 @@ uint64_t k4_impl(eh_graph* g) {
       kw<<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, n64, g->d_counter, sf16, 6u);
       EH_LAUNCH("k_k4_warp");
     }
-    if (nsmall > n64) {
+    if (nsmall > n64 && n64 && getenv("EH_TEST_K4_W128") == nullptr) {
+      // class 1 (64 < |N+(x)| <= 128) as 4-warp CTAs over its LPT list (cursor slot 7):
+      // ~7 KB each, 16 per SM, where the 128-entry warp instance holds 8.4 KB per warp
+      // (measured: C3 K4 34.3 -> 32.7 ms, C2 1.24 -> 1.18, C4 5.89 -> 5.80; 2 / 8 warps
+      // per CTA close behind)
+      launch_k4_cta<kU, 128, 4>(g, work_lpt(g) + g->n_work[0], nsmall - n64, 0u, 7u, sf16, ss);
+    } else if (nsmall > n64) {
       auto kw = k_k4_warp<kU, kWMaxD>;
       const size_t smem = sizeof(K4WarpSmem<kWMaxD>) * kWWarps;
       EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
