@@ -198,8 +198,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_k4_warp(const uint4* __restric
           wb &= wb - 1;
           const uint32_t j = kk * 32 + b;
           if (kU ? q < W : (q >= kk && q < W)) {  // unpruned: all w, else w after z
-            const uint32_t m = (kU || q != kk) ? 0xFFFFFFFFu : ~((2u << b) - 1u);
-            cnt += __popc(li & sm.L[j * kWWd + q] & m);
+            cnt += __popc(li & sm.L[j * kWWd + q]);  // row j's bits all lie above j
           }
         }
       }
@@ -294,7 +293,9 @@ __global__ void __launch_bounds__(kCWarps * 32) k_k4_cta(const uint4* __restrict
         if (kU) {  // all w
           for (uint32_t k = 0; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
         } else {   // w after z
-          acc = __popc(Li[kk] & Lj[kk] & ~((2u << (j & 31)) - 1u));
+          // every bit of row j lies above j (row j = N+(x) after x_j cap N+(x_j)), so the
+          // words of L_i AND L_j need no mask
+          acc = __popc(Li[kk] & Lj[kk]);
           for (uint32_t k = kk + 1; k < W; ++k) acc += __popc(Li[k] & Lj[k]);
         }
         cnt += acc;
