@@ -401,17 +401,30 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   const uint32_t b = std::max<uint32_t>(1, bitlen(n_ids - 1));
   const uint64_t sentinel = (b >= 32) ? ~0ull : ((1ull << (2 * b)) - 1ull);
 
-  // ---- a1-a3: canonical keys, deduplicated.  Default: radix sort over the 2b
-  // significant bits, then unique adjacent keys.  EH_TEST_DEDUP=hash selects a fused
-  // canonicalise + GPU hash-set insert (load <= ~0.6) and a compaction of the
-  // occupied slots (the downstream steps only need the DISTINCT edges); it was
-  // measured slower on C3 (random DRAM sectors, and the unsorted output slows
-  // the CSR scatter), so it is kept as an ablation.
+  // ---- a1-a4: canonical keys, deduplicated, and the degree of every id.
+  // Default: the bucketed pass of dedup.cu (one MSD radix digit of the low end, an
+  // on-chip hash set per bucket; the degrees come out of the same pass).  Test hook
+  // EH_TEST_DEDUP=sort: LSD radix sort over the 2b significant bits, unique adjacent
+  // keys, degrees from the sorted runs (round-1 default, kept as an ablation and as
+  // the path for ids of 32 bits); EH_TEST_DEDUP=hash: one global hash set.
+  static const int dd_mode = [] {
+    const char* e = getenv("EH_TEST_DEDUP");
+    return !e ? 0 : (strcmp(e, "sort") == 0 ? 1 : (strcmp(e, "hash") == 0 ? 2 : 0));
+  }();
   uint64_t m = 0, nk = 0;  // nk key entries; m of them are distinct non-loop edges
   DBuf<uint64_t> keys, alt;
   uint64_t* ukeys = nullptr;
-  const char* dd_env = getenv("EH_TEST_DEDUP");
-  if (!(dd_env && strcmp(dd_env, "hash") == 0)) {
+  DBuf<uint32_t> deg(al, n_ids);
+  EH_CUDA(cudaMemsetAsync(deg.p, 0, n_ids * 4, s));
+  DBuf<unsigned long long> dm(al, 3);  // {m, max degree, n_act}: one host read
+  EH_CUDA(cudaMemsetAsync(dm.p, 0, 24, s));
+  const bool bucketed = dd_mode == 0 && bucket_dedup_ok(b, n);
+  if (bucketed) {
+    keys = DBuf<uint64_t>(al, n);  // m <= n distinct keys, compact
+    bucket_dedup(usrc, udst, n, b, deg.p, dm.p, keys.p, g);
+    ukeys = keys.p;
+    mark("dedup");
+  } else if (dd_mode != 2) {
     keys = DBuf<uint64_t>(al, n);
     alt = DBuf<uint64_t>(al, n);
     // a1 canonicalisation fused into the sort's histogram and first pass; the
@@ -434,14 +447,10 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   }
   msrc.reset();
   mdst.reset();
-  mark("dedup");
+  if (!bucketed) mark("dedup");
 
   // ---- a4: degree + (degree, id) rank
-  DBuf<uint32_t> deg(al, n_ids);
-  EH_CUDA(cudaMemsetAsync(deg.p, 0, n_ids * 4, s));
-  DBuf<unsigned long long> dm(al, 3);  // {m, max degree, n_act}: one host read
-  EH_CUDA(cudaMemsetAsync(dm.p, 0, 24, s));
-  if (nk) {
+  if (nk && !bucketed) {
     k_degree<<<grid_for(nk, TB * 4), TB, 0, s>>>(ukeys, nk, b, sentinel, deg.p, dm.p);
     EH_LAUNCH("k_degree");
   }
@@ -452,6 +461,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   EH_CUDA(cudaStreamSynchronize(s));
   m = hm[0];
   g->m = m;
+  if (bucketed) nk = m;
   const uint32_t max_deg = (uint32_t)hm[1];
   const uint64_t n_act = hm[2];
   // NEXT-4: the primary rank key of the chosen node ordering (default: degree)

@@ -223,16 +223,38 @@ def test_layout_and_binning_invariance(kw):
     assert _gpu_counts(src, dst, **kw)[:2] == base
 
 
+@pytest.mark.parametrize("mode", ["hash", "sort"])
 @pytest.mark.parametrize("seed", range(3))
-def test_hash_dedup_path(seed, monkeypatch):
-    """EH_TEST_DEDUP=hash: canonical keys deduplicated by a GPU hash set instead of
-    the one-sweep radix sort -- same trie, same counts."""
+def test_dedup_ablation_paths(seed, mode, monkeypatch):
+    """EH_TEST_DEDUP=hash (one global hash set) and EH_TEST_DEDUP=sort (the one-sweep
+    radix sort of the canonical keys) instead of the bucketed on-chip dedup of
+    dedup.cu -- same trie, same counts."""
     src, dst = synth.rmat(13, 16, 70 + seed)
     base = _gpu_counts(src, dst)
-    monkeypatch.setenv("EH_TEST_DEDUP", "hash")
+    monkeypatch.setenv("EH_TEST_DEDUP", mode)
     alt = _gpu_counts(src, dst)
     assert base[:2] == alt[:2] == (oracle.count_triangles(src, dst), oracle.count_4cliques(src, dst))
     assert base[2] == alt[2]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_bucket_classes_with_duplicates(seed):
+    """Buckets of every dedup class (shared-memory tables of the small and big CTAs,
+    global tables above 36,000 pairs) with heavy duplication and both orientations of
+    each pair: hubs whose pairs fill one bucket, plus RMAT background."""
+    rng = np.random.default_rng(seed)
+    bs, bd = synth.rmat(14, 8, 900 + seed)
+    parts_s, parts_d = [bs], [bd]
+    for hub, k, rep in ((3, 60_000, 3), (70_000, 12_000, 2), (5, 3_000, 4)):
+        nb = rng.choice(1 << 17, size=k, replace=False).astype(np.uint32)
+        nb = np.repeat(nb, rep)
+        flip = rng.random(nb.size) < 0.5
+        parts_s.append(np.where(flip, nb, hub).astype(np.uint32))
+        parts_d.append(np.where(flip, hub, nb).astype(np.uint32))
+    s = np.concatenate(parts_s)
+    d = np.concatenate(parts_d)
+    perm = rng.permutation(s.size)
+    _check(s[perm], d[perm])
 
 
 def test_device_input_and_stream():
