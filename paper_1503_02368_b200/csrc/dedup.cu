@@ -36,7 +36,7 @@ namespace {
 
 constexpr uint32_t kEmptyR = 0xFFFFFFFFu;  // residuals have <= 31 bits
 constexpr int kMaxLoBits = 12;             // <= 4096 lo values per bucket (shared-memory counters)
-constexpr int kHistSmemBits = 14;          // shared-memory histogram up to 2^14 buckets
+constexpr int kHistSmemBits = 15;          // shared-memory histogram up to 2^15 buckets (128 KB, one CTA per SM)
 constexpr int kSmallThreads = 512;
 constexpr uint32_t kSmallSlots = 16384;    // 64 KB table: buckets of <= kSmallMax pairs
 constexpr uint32_t kSmallMax = 8192;
@@ -93,7 +93,7 @@ __device__ __forceinline__ void for_pairs(const uint32_t* __restrict__ src, cons
 
 // (1) bucket histogram; kSmem: per-CTA shared-memory counters, else warp-aggregated global atomics
 template <bool kSmem>
-__global__ void __launch_bounds__(256) k_bkt_hist(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+__global__ void __launch_bounds__(1024) k_bkt_hist(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
                                                   uint64_t n, BktParams p, uint32_t nb, uint32_t* __restrict__ cnt) {
   extern __shared__ uint32_t sh_hist[];
   if (kSmem) {
@@ -139,6 +139,49 @@ __global__ void __launch_bounds__(256) k_bkt_part(const uint32_t* __restrict__ s
       part[boff[bk] + p0 + __popc(peers & lt)] = r;
     }
   });
+}
+
+// (3') the same without warp aggregation: with >= 2^13 buckets a warp's 32 pairs
+// rarely share one, so the match costs more than the atomics it saves; the four
+// pairs of a 128-bit load issue their cursor atomics back to back; cur[] starts at the
+// buckets' absolute offsets (k_bkt_cursors)
+__global__ void __launch_bounds__(256) k_bkt_part_direct(const uint32_t* __restrict__ src,
+                                                         const uint32_t* __restrict__ dst, uint64_t n, BktParams p,
+                                                         const uint64_t* __restrict__ boff, uint32_t* __restrict__ cur,
+                                                         uint32_t* __restrict__ part) {
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    const uint4* d4 = reinterpret_cast<const uint4*>(dst);
+    const uint64_t n4 = n / 4;
+    for (uint64_t i = t0; i < n4; i += nt) {
+      const uint4 a = __ldcs(s4 + i), c = __ldcs(d4 + i);
+      const uint32_t u[4] = {a.x, a.y, a.z, a.w}, v[4] = {c.x, c.y, c.z, c.w};
+      uint32_t bk[4], r[4], q[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ok[k] = pair_bucket(u[k], v[k], p, bk[k], r[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = ok[k] ? atomicAdd(&cur[bk[k]], 1u) : 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ok[k]) {
+          EH_DASSERT(q[k] >= boff[bk[k]] && q[k] < boff[bk[k] + 1]);
+          part[q[k]] = r[k];
+        }
+    }
+    done = n4 * 4;
+  }
+  for (uint64_t i = done + t0; i < n; i += nt) {
+    uint32_t bk, r;
+    if (pair_bucket(src[i], dst[i], p, bk, r)) part[atomicAdd(&cur[bk], 1u)] = r;
+  }
+}
+
+// cursors of k_bkt_part_direct: absolute positions (n < 2^32), so the scatter needs no offset load
+__global__ void k_bkt_cursors(const uint64_t* __restrict__ boff, uint32_t nb, uint32_t* __restrict__ cur) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += gridDim.x * blockDim.x) cur[k] = (uint32_t)boff[k];
 }
 
 // (4a) bucket classes by size: 0 shared-memory table (small CTA), 1 shared-memory
@@ -273,12 +316,13 @@ bool bucket_dedup_ok(uint32_t b, uint64_t n) {
 // a1-a4: distinct canonical keys into `out` (compact, m entries, grouped by bucket
 // and lo), deg[id] += distinct neighbours (deg zeroed by the caller), *m_ctr += m.
 void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t b, uint32_t* deg,
-                  unsigned long long* m_ctr, uint64_t* out, eh_graph* g) {
+                  unsigned long long* m_ctr, uint64_t* out, eh_graph* g, PhaseTimer* tm) {
   Allocator& al = g->alloc;
   cudaStream_t s = g->stream;
   // bb bucket bits: residual <= 31 bits, <= 2^12 lo values per bucket, ~4096 pairs per bucket
   int bb = std::max<int>(2 * (int)b - 31, (int)b - kMaxLoBits);
   bb = std::max<int>(bb, (int)bitlen(n >> 12));
+  if (const char* e = getenv("EH_TEST_BKT_SHIFT")) bb = std::max<int>(2 * (int)b - 31, bb + atoi(e));  // test hook
   bb = std::max(0, std::min<int>(bb, (int)b));
   const BktParams p{b, b - (uint32_t)bb};
   const uint32_t nb = 1u << bb;
@@ -287,10 +331,12 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   EH_CUDA(cudaMemsetAsync(cur.p, 0, nb * 4ull, s));
   const unsigned TB = 256;
   const unsigned grid_stream = grid_for((n + 3) / 4, TB, kSMs * 8);
-  if (bb <= kHistSmemBits) {
+  if (bb <= kHistSmemBits && getenv("EH_TEST_BKT_GHIST") == nullptr) {
     const size_t sm = nb * 4ull;
     if (sm > 48 * 1024) EH_CUDA(cudaFuncSetAttribute(k_bkt_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_bkt_hist<true><<<grid_stream, TB, sm, s>>>(src, dst, n, p, nb, cnt.p);
+    // 1024-thread CTAs, as many per SM as the counters allow (one at 2^15 buckets)
+    const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / std::max<size_t>(sm, 1)));
+    k_bkt_hist<true><<<std::min(grid_for((n + 3) / 4, 1024), kSMs * per_sm), 1024, sm, s>>>(src, dst, n, p, nb, cnt.p);
   } else {
     k_bkt_hist<false><<<grid_stream, TB, 0, s>>>(src, dst, n, p, nb, cnt.p);
   }
@@ -299,8 +345,16 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   scan_exclusive_u32(cnt.p, boff.p, nb, tot.p, al, s);
   EH_CUDA(cudaMemcpyAsync(boff.p + nb, tot.p, 8, cudaMemcpyDeviceToDevice, s));
   DBuf<uint32_t> part(al, n);
-  k_bkt_part<<<grid_stream, TB, 0, s>>>(src, dst, n, p, boff.p, cur.p, part.p);
+  if (tm) tm->mark("bkt_hist");
+  if (getenv("EH_TEST_BKT_PART_MATCH") == nullptr) {
+    k_bkt_cursors<<<grid_for(nb, TB), TB, 0, s>>>(boff.p, nb, cur.p);
+    EH_LAUNCH("k_bkt_cursors");
+    k_bkt_part_direct<<<grid_stream, TB, 0, s>>>(src, dst, n, p, boff.p, cur.p, part.p);
+  } else {
+    k_bkt_part<<<grid_stream, TB, 0, s>>>(src, dst, n, p, boff.p, cur.p, part.p);
+  }
   EH_LAUNCH("k_bkt_part");
+  if (tm) tm->mark("bkt_part");
   cur.reset();
   DBuf<uint32_t> lists(al, 3ull * nb);
   DBuf<uint64_t> gtab(al, nb);

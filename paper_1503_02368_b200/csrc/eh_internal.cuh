@@ -264,7 +264,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
 // dedup.cu: the bucketed a1-a4 pass (distinct keys, compact; degrees; *m_ctr += m)
 bool bucket_dedup_ok(uint32_t b, uint64_t n);
 void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t b, uint32_t* deg,
-                  unsigned long long* m_ctr, uint64_t* out, eh_graph* g);
+                  unsigned long long* m_ctr, uint64_t* out, eh_graph* g, PhaseTimer* tm = nullptr);
 // trie.cu: set-level layout (uint / bitset) and the bitset pool; work lists.
 void build_layouts(eh_graph* g);
 const uint32_t* work_lpt(eh_graph* g);  // lazy: LPT-ordered work lists (trie.cu)

@@ -377,6 +377,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   k_max_id<<<grid_for(n, TB * 8), TB, 0, s>>>(d_src, d_dst, n, dmax.p);
   EH_LAUNCH("k_max_id");
   const uint32_t max_id = read_scalar(dmax.p, s);
+  mark("max_id");
   uint64_t n_ids = (uint64_t)max_id + 1;
   DBuf<uint32_t> dict, msrc, mdst;
   const uint32_t* usrc = d_src;
@@ -421,7 +422,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   const bool bucketed = dd_mode == 0 && bucket_dedup_ok(b, n);
   if (bucketed) {
     keys = DBuf<uint64_t>(al, n);  // m <= n distinct keys, compact
-    bucket_dedup(usrc, udst, n, b, deg.p, dm.p, keys.p, g);
+    bucket_dedup(usrc, udst, n, b, deg.p, dm.p, keys.p, g, tm);
     ukeys = keys.p;
     mark("dedup");
   } else if (dd_mode != 2) {
