@@ -54,6 +54,9 @@ enum {
 #define EH_BLOCK_LAYOUT    0x10u /* NEXT-3 block-level (composite) layout for eh_count_triangles:
                                     every set is split into 128-id blocks; blocks with >= 4 elements are bitset
                                     blocks, the rest stay uint (the set-level layouts serve the other queries) */
+#define EH_FORCE_SEARCH    0x20u /* ablation / microbenchmark: EH_ALL_UINT and every uint cap uint row takes the
+                                   * galloping (binary-search) side, whatever the cardinalities -- the opposite of
+                                   * EH_NO_ALGO; with both, EH_NO_ALGO wins (Fig. `fig:card_skew2`) */
 #define EH_NO_ALGO         0x8u /* the paper's "-RA" ablation (NEXT-3): EH_ALL_UINT and no
                                    intersection-algorithm choice (every uint cap uint streams, no galloping) */
 
@@ -76,7 +79,7 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* stream, void* ctx);
   void (*dev_free)(void* ptr, void* stream, void* ctx);
   void* alloc_ctx;
-  uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT */
+  uint32_t flags;          /* EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT | EH_FORCE_SEARCH */
   /* Count-kernel work classes by d = |N+(x)|: 0 = [2, bin_small_max], 1 = up to
    * bin_large_min - 1, 2 = the rest.  Triangle / per-vertex kernels: class 0 warp-per-x,
    * classes 1-2 CTA-per-x; 4-clique kernels: classes 0-1 warp-per-x, class 2 CTA-per-x.
@@ -106,7 +109,11 @@ enum {
   EH_ORDER_RANDOM = 2,     /* a fixed pseudo-random permutation of the ids */
   EH_ORDER_BFS = 3,        /* breadth-first from the highest-degree vertex (level, then id) */
   EH_ORDER_HYBRID = 4,     /* BFS labels, then stably sorted by descending degree */
-  EH_ORDER_SHINGLE = 5     /* by neighbourhood min-hash (shingle), then id */
+  EH_ORDER_SHINGLE = 5,    /* by neighbourhood min-hash (shingle), then id */
+  EH_ORDER_ID = 6          /* the ids as given: ranks ascend by (dictionary-encoded) input id, edges point low -> high
+                            * id.  Not one of the paper's orderings: it lets a caller fix the orientation, which the
+                            * intersection microbenchmarks (tools/intersect_bench.py) use
+                            * to build rows |A cap B| of chosen cardinality, range and layout. */
 };
 
 /* eh_stats: filled by eh_graph_stats (bench / tests). */

@@ -79,7 +79,7 @@ __device__ __forceinline__ uint8_t k4_kind(const YInfo& y, uint32_t a, uint32_t 
   if (a == 0 || y.len == 0) return kKSkip;
   if (y.c1 > y.c0) return kKProbe;
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kKSearch;  // sf16: see count_tri.cu row_kind
+  if (y.c0 >= kAlwaysSearch ? y.c0 == kAlwaysSearch : (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kKSearch;  // sf16: see count_tri.cu row_kind
   return kKStream;
 }
 
@@ -483,7 +483,7 @@ void launch_k4_cta(eh_graph* g, const uint32_t* wl, uint64_t nlarge, uint32_t dl
                    cudaStream_t st) {
   constexpr size_t smem = k4_cta_smem<kMaxD, kCWarps>();
   auto k = k_k4_cta<kU, kMaxD, kCWarps>;
-  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCWarps * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
@@ -515,7 +515,7 @@ uint64_t k4_impl(eh_graph* g) {
     if (n64) {
       auto kw = k_k4_warp<kU, 64>;
       const size_t smem = sizeof(K4WarpSmem<64>) * kWWarps;
-      EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_dyn_smem((const void*)kw, smem);
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kw, kWWarps * 32, smem));
       const unsigned grid = (unsigned)std::min<uint64_t>((n64 + kWWarps - 1) / kWWarps, (uint64_t)kSMs * std::max(1, per_sm));
@@ -531,7 +531,7 @@ uint64_t k4_impl(eh_graph* g) {
     } else if (nsmall > n64) {
       auto kw = k_k4_warp<kU, kWMaxD>;
       const size_t smem = sizeof(K4WarpSmem<kWMaxD>) * kWWarps;
-      EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_dyn_smem((const void*)kw, smem);
       const unsigned grid = (unsigned)std::min<uint64_t>((nsmall - n64 + kWWarps - 1) / kWWarps, (uint64_t)kSMs * 8);
       kw<<<grid, kWWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work + n64, nsmall - n64, g->d_counter, sf16,
                                             1u);
@@ -568,7 +568,7 @@ uint64_t k4_impl(eh_graph* g) {
       // P's bitmap over all ids on chip when it fits next to the P list (C2: 32 KB, C4: 80 KB)
       const uint32_t bm_words = (g->n_act + 127) / 128 * 4 <= kBigBmMaxWords ? (uint32_t)((g->n_act + 127) / 128 * 4) : 0u;
       const size_t smem = ((size_t)kBigPCap + bm_words) * 4;
-      EH_CUDA(cudaFuncSetAttribute(k_k4_big<kU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_dyn_smem((const void*)k_k4_big<kU>, smem);
       int per_sm = 0;
       EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_k4_big<kU>, kBigThreads, smem));
       const unsigned gb = (unsigned)std::min<uint64_t>(nrows, (uint64_t)kSMs * std::max(1, per_sm));

@@ -140,7 +140,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XI
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearch;  // sf16: see count_tri.cu row_kind
+  if (y.c0 >= kAlwaysSearch ? y.c0 == kAlwaysSearch : (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearch;  // sf16: see count_tri.cu row_kind
   return kStream;
 }
 
@@ -427,7 +427,7 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
                                               : xcap;                                         // the unstaged path
     const size_t smem = cta_smem(xc);
     auto kc = k_pv_cta<kPiv>;  // 8 warps (4 / 16 measured slower: C3 17.3 / 16.6 ms)
-    EH_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem((const void*)kc, smem);
     int per_sm = 0;
     EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, kCtaWarps * 32, smem));
     const unsigned grid = (unsigned)std::min<uint64_t>(nlarge, (uint64_t)kSMs * std::max(1, per_sm));
@@ -438,7 +438,7 @@ static void pv_launch(eh_graph* g, unsigned long long* d_t, uint32_t sf16) {
     const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWarps - 1) / kWarps, (uint64_t)kSMs * 8);
     const size_t smem = sizeof(PvWarpSmem) * kWarps;
     auto kw = k_pv_warp<kPiv>;
-    EH_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem((const void*)kw, smem);
     kw<<<grid, kWarps * 32, smem, ss>>>(g->desc, g->col, g->bs, g->work, nsmall, d_t, sf16, g->d_counter);
     EH_LAUNCH("k_pv_warp");
   }

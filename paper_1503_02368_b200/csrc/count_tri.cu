@@ -56,7 +56,13 @@ constexpr uint32_t kAndFactor = 8;    // AND when overlap chunks <= kAndFactor *
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 enum RowKind : uint8_t { kSkip = 0, kProbe = 1, kAnd = 2, kStream = 3, kSearchGlobal = 4 };
-enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2 };
+enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2, kHashF = 3 };
+#ifndef EH_HASH_FILTER
+#define EH_HASH_FILTER 1
+#endif
+#ifndef EH_HASH_FILTER_MUL
+#define EH_HASH_FILTER_MUL 4
+#endif
 
 // ---------------------------------------------- x's membership structure --
 // N+(x) in shared memory as (a) an exact bitmap over [lo, lo + nbits), (b) an
@@ -73,6 +79,19 @@ struct XSet {
       return (o < nbits) ? (tab[o >> 5] >> (o & 31)) & 1u : 0u;
     }
     if (e < amin || e > amax) return 0u;
+    if (mode == kHashF) {
+      // filter word w = the hash slot's home index: one bit per (w, next 5 hash bits)
+      const uint32_t h = e * 2654435761u;
+      uint32_t s = h >> hshift;
+      if (!((tab[s] >> ((h >> (hshift - 5)) & 31)) & 1u)) return 0u;
+      const uint32_t* slots = tab + hmask + 1;
+      for (;;) {
+        const uint32_t v = slots[s];
+        if (v == e) return 1u;
+        if (v == kEmpty) return 0u;
+        s = (s + 1) & hmask;
+      }
+    }
     if (mode == kHash) {
       uint32_t s = (e * 2654435761u) >> hshift;
       for (;;) {
@@ -110,6 +129,14 @@ __device__ __forceinline__ XSet plan_xset(uint32_t* tab, uint32_t tab_words, con
     s.lo = lo;
     s.nbits = (uint32_t)span_bits;
     s.hshift = s.hmask = 0;
+  } else if (EH_HASH_FILTER && tab_words >= 64 && EH_HASH_FILTER_MUL * d <= tab_words) {
+    // half the budget as a one-hash filter (16 * tab_words bits, <= d of them set), half as
+    // the hash table (load <= 1/2): a miss -- most lookups -- costs one load and never probes
+    const uint32_t half = tab_words / 2;  // a power of two
+    s.mode = kHashF;
+    s.lo = s.nbits = 0;
+    s.hshift = 32 - (31 - __clz(half));
+    s.hmask = half - 1u;
   } else if ((1u << hbits) <= tab_words && (1u << hbits) >= 2 * d) {
     s.mode = kHash;
     s.lo = s.nbits = 0;
@@ -131,6 +158,8 @@ __device__ __forceinline__ void fill_xset(const XSet& s, int tid, int nthreads) 
     for (uint32_t k = tid; k < s.nbits / 32; k += nthreads) tab[k] = 0u;
   } else if (s.mode == kHash) {
     for (uint32_t k = tid; k <= s.hmask; k += nthreads) tab[k] = kEmpty;
+  } else if (s.mode == kHashF) {
+    for (uint32_t k = tid; k <= s.hmask; k += nthreads) { tab[k] = 0u; tab[s.hmask + 1 + k] = kEmpty; }
   }
   if (nthreads == 32) __syncwarp(); else __syncthreads();
   const uint32_t lo = s.lo;
@@ -145,6 +174,15 @@ __device__ __forceinline__ void fill_xset(const XSet& s, int tid, int nthreads) 
       const uint32_t e = xs[k];
       uint32_t h = (e * 2654435761u) >> s.hshift;
       while (atomicCAS(&tab[h], kEmpty, e) != kEmpty) h = (h + 1) & s.hmask;
+    }
+  } else if (s.mode == kHashF) {
+    uint32_t* slots = tab + s.hmask + 1;
+    for (uint32_t k = tid; k < d; k += nthreads) {
+      const uint32_t e = xs[k];
+      const uint32_t hh = e * 2654435761u;
+      uint32_t h = hh >> s.hshift;
+      atomicOr(&tab[h], 1u << ((hh >> (s.hshift - 5)) & 31));
+      while (atomicCAS(&slots[h], kEmpty, e) != kEmpty) h = (h + 1) & s.hmask;
     }
   }
 }
@@ -176,7 +214,7 @@ __device__ __forceinline__ uint8_t row_kind(const YInfo& y, uint32_t a, const XS
     return kProbe;
   }
   const uint32_t lg = 32 - __clz(y.len);
-  if (y.c0 != kNoAlgo && (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearchGlobal;
+  if (y.c0 >= kAlwaysSearch ? y.c0 == kAlwaysSearch : (uint64_t)a * lg * sf16 < (uint64_t)y.len * 16) return kSearchGlobal;
   return kStream;
 }
 
@@ -199,7 +237,7 @@ __device__ __forceinline__ uint8_t row_kind_unpruned(const YInfo& y, uint32_t a,
     return (stream < a) ? kStream : kProbe;
   }
   const uint64_t search = (uint64_t)a * (32 - __clz(y.len)) * sf16;
-  return (y.c0 != kNoAlgo && search < stream * 16) ? kSearchGlobal : kStream;
+  return (y.c0 >= kAlwaysSearch ? y.c0 == kAlwaysSearch : search < stream * 16) ? kSearchGlobal : kStream;
 }
 
 // ---- group-level row bodies: kG lanes, gl = lane within the group --------
@@ -795,7 +833,7 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
     k_item_emit<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->work + nsmall, nlarge, cnt.p, off.p, items.p);
     EH_LAUNCH("k_item_emit");
   }
-  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>(nitems, (uint64_t)kSMs * std::max(1, per_sm));
@@ -815,7 +853,7 @@ void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, u
   if (!work) work = g->work;
   auto k = k_tri_warp<kUnpruned, kBlock, kMaxD, kMinB, kWG, kSF, kPiv>;
   const size_t smem = sizeof(WarpSmem<kMaxD>) * kWK_Warps;
-  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWK_Warps * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>((nsmall + kWK_Warps - 1) / kWK_Warps,

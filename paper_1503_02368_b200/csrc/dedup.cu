@@ -297,7 +297,7 @@ void launch_dedup(uint64_t nlist, size_t smem, const uint32_t* part, const uint6
                   uint64_t* out, uint32_t* gscr, const uint64_t* gtab, cudaStream_t s) {
   if (nlist == 0) return;
   auto k = k_bkt_dedup<kThreads, kMode, kSlots>;
-  if (smem > 48 * 1024) EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   int per_sm = 1;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem));
   const uint64_t grid = std::min<uint64_t>(nlist, (uint64_t)kSMs * std::max(1, per_sm));
@@ -333,7 +333,7 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   const unsigned grid_stream = grid_for((n + 3) / 4, TB, kSMs * 8);
   if (bb <= kHistSmemBits && getenv("EH_TEST_BKT_GHIST") == nullptr) {
     const size_t sm = nb * 4ull;
-    if (sm > 48 * 1024) EH_CUDA(cudaFuncSetAttribute(k_bkt_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ensure_dyn_smem((const void*)k_bkt_hist<true>, sm);
     // 1024-thread CTAs, as many per SM as the counters allow (one at 2^15 buckets)
     const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / std::max<size_t>(sm, 1)));
     k_bkt_hist<true><<<std::min(grid_for((n + 3) / 4, 1024), kSMs * per_sm), 1024, sm, s>>>(src, dst, n, p, nb, cnt.p);

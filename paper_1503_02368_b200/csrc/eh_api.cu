@@ -7,10 +7,25 @@
 
 #include <cstring>
 #include <exception>
+#include <map>
+#include <mutex>
 #include <thread>
 
 namespace eh {
 std::atomic<unsigned long long> g_launches{0};
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;  // within the default limit
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limit;
+  int dev = 0;
+  EH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = limit[{dev, kernel}];
+  if (bytes <= cur) return;
+  EH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
+}
 
 SideStreams& side_streams(int device) {
   constexpr int kMaxDev = 64;
@@ -94,7 +109,7 @@ eh_graph* load_impl(const uint32_t* src, const uint32_t* dst, uint64_t n, const 
     if (n && (!src || !dst)) eh::fail(EH_EINVAL, "eh_load_edges: NULL src/dst with n = %llu", (unsigned long long)n);
     if ((c.dev_alloc == nullptr) != (c.dev_free == nullptr))
       eh::fail(EH_EINVAL, "eh_load_edges: dev_alloc and dev_free must be set together");
-    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT))
+    if (c.flags & ~(uint32_t)(EH_INPUT_ON_DEVICE | EH_SET_DEVICE | EH_ALL_UINT | EH_NO_ALGO | EH_BLOCK_LAYOUT | EH_FORCE_SEARCH))
       eh::fail(EH_EINVAL, "eh_load_edges: unknown flags 0x%x", c.flags);
     int ndev = 0;
     EH_CUDA(cudaGetDeviceCount(&ndev));
@@ -109,13 +124,13 @@ eh_graph* load_impl(const uint32_t* src, const uint32_t* dst, uint64_t n, const 
     eh_graph* g = new eh_graph();
     try {
       g->device = dev;
-      g->flags = c.flags | ((c.flags & EH_NO_ALGO) ? EH_ALL_UINT : 0u);  // -RA implies -R
+      g->flags = c.flags | ((c.flags & (EH_NO_ALGO | EH_FORCE_SEARCH)) ? EH_ALL_UINT : 0u);  // -RA implies -R
       g->tau = c.bitset_tau ? c.bitset_tau : 128;
       g->min_bitset_card = c.min_bitset_card ? c.min_bitset_card : 2;
       g->bin_small_max = c.bin_small_max;
       g->bin_large_min = c.bin_large_min;
       g->bin_thread_max = c.bin_thread_max;
-      if (c.order > EH_ORDER_SHINGLE) eh::fail(EH_EINVAL, "eh_load_edges: unknown order %u", c.order);
+      if (c.order > EH_ORDER_ID) eh::fail(EH_EINVAL, "eh_load_edges: unknown order %u", c.order);
       g->order = c.order;
       if (c.stream) {
         g->stream = (cudaStream_t)c.stream;

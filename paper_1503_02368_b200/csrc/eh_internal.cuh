@@ -51,6 +51,11 @@ extern std::atomic<unsigned long long> g_launches;
   (::eh::g_launches.fetch_add(1, std::memory_order_relaxed), \
    ::eh::check_cuda(cudaGetLastError(), what, __FILE__, __LINE__))
 
+// Raises a kernel's dynamic shared-memory limit to at least `bytes` on the current device.
+// The limit only ever grows (per device and kernel): two host threads launching the same
+// kernel with different sizes (eh_count_batch's lanes) cannot lower it under each other.
+void ensure_dyn_smem(const void* kernel, size_t bytes);
+
 // Device allocator: the caller's hooks (e.g. torch's caching allocator) or cudaMallocAsync.
 // Default device allocation path (no allocator hook): cudaMallocAsync on the
 // handle's stream, with a process-wide cache of large blocks (>= 4 MB, sizes

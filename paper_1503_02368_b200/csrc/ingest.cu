@@ -485,6 +485,8 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
       pbits = (g->order == EH_ORDER_BFS) ? aux_bits : bitlen(max_deg) + aux_bits;
     } else if (g->order == EH_ORDER_RANDOM) {
       pbits = 32;
+    } else if (g->order == EH_ORDER_ID) {
+      pbits = 1;  // primary 0 everywhere: ranks ascend by id
     }
     if (b + pbits > 64) fail(EH_EINVAL, "node ordering key needs %u bits", b + pbits);
     k_prim_simple<<<grid_for(n_ids, TB * 4), TB, 0, s>>>(deg.p, n_ids, g->order, max_deg, aux.p, aux_max, aux_bits,

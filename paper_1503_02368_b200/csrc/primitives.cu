@@ -300,7 +300,7 @@ template <typename K, int kBits, int kPBlock, int kRItems, bool kCanon>
 static void launch_pass(const K* src, CanonSrc cs, K* dst, uint64_t n, uint32_t shift, const unsigned long long* bp,
                         unsigned long long* status, uint32_t* ctr, uint64_t tiles, size_t smem, cudaStream_t s) {
   auto k = k_radix_pass<K, kBits, kPBlock, kRItems, kCanon>;
-  EH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem((const void*)k, smem);
   k<<<(unsigned)tiles, kPBlock, smem, s>>>(src, cs, dst, n, shift, bp, status, ctr);
   EH_LAUNCH("k_radix_pass");
 }

@@ -11,6 +11,8 @@ namespace eh {
 // desc[v].w of every set of an EH_NO_ALGO graph (all uint): row dispatch never
 // chooses the galloping (binary-search) side -- the paper's "-RA" ablation.
 constexpr uint32_t kNoAlgo = 0xFFFFFFFFu;
+// EH_FORCE_SEARCH (all uint): row dispatch always chooses the galloping side.
+constexpr uint32_t kAlwaysSearch = 0xFFFFFFFEu;
 
 struct YInfo {
   uint32_t list;  // col offset of N+(y) in 16-B units

@@ -42,13 +42,14 @@ __global__ void k_layout(const uint4* __restrict__ desc, const uint32_t* __restr
   }
 }
 
-// no_algo (EH_NO_ALGO, the "-RA" ablation): every set is uint and its first-chunk
-// field carries kNoAlgo, which the row dispatch reads as "never gallop".
+// marker (EH_NO_ALGO, the "-RA" ablation / EH_FORCE_SEARCH): every set is uint and its
+// first-chunk field carries kNoAlgo / kAlwaysSearch, which the row dispatch reads as
+// "never gallop" / "always gallop".
 __global__ void k_desc_layout(uint4* __restrict__ desc, const uint64_t* __restrict__ bs_off,
-                              const uint32_t* __restrict__ chunk0, uint64_t n_act, uint64_t total, bool no_algo) {
+                              const uint32_t* __restrict__ chunk0, uint64_t n_act, uint64_t total, uint32_t marker) {
   for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n_act; v += (uint64_t)gridDim.x * blockDim.x) {
     desc[v].z = (uint32_t)(v < n_act ? bs_off[v] : total);
-    desc[v].w = (v < n_act) ? (no_algo ? kNoAlgo : chunk0[v]) : 0u;
+    desc[v].w = (v < n_act) ? (marker ? marker : chunk0[v]) : 0u;
   }
 }
 
@@ -247,7 +248,8 @@ void build_layouts(eh_graph* g) {
   scan_exclusive_u32(nch.p, off.p, n, tot.p, al, s);
   const uint64_t total = read_scalar(tot.p, s);
   if (total >= (1ull << 32)) fail(EH_EINVAL, "bitset pool too large (%llu chunks)", (unsigned long long)total);
-  k_desc_layout<<<grid_for(n + 1, TB * 4), TB, 0, s>>>(g->desc, off.p, c0.p, n, total, (g->flags & EH_NO_ALGO) != 0);
+  k_desc_layout<<<grid_for(n + 1, TB * 4), TB, 0, s>>>(g->desc, off.p, c0.p, n, total,
+                                                       (g->flags & EH_NO_ALGO) ? kNoAlgo : (g->flags & EH_FORCE_SEARCH) ? kAlwaysSearch : 0u);
   EH_LAUNCH("k_desc_layout");
   g->bs_words = total * 4;
   g->bs = (uint32_t*)g->own(std::max<uint64_t>(16, total * 16));

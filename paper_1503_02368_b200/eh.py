@@ -26,7 +26,7 @@ if os.environ.get("EH_LIB") == "checked":
 
 EH_OK, EH_EINVAL, EH_ENOMEM, EH_ECUDA, EH_EUNSORTED = 0, -1, -2, -3, -4
 EH_COUNT_ERROR = 2**64 - 1
-EH_INPUT_ON_DEVICE, EH_SET_DEVICE, EH_ALL_UINT, EH_NO_ALGO, EH_BLOCK_LAYOUT = 0x1, 0x2, 0x4, 0x8, 0x10
+EH_INPUT_ON_DEVICE, EH_SET_DEVICE, EH_ALL_UINT, EH_NO_ALGO, EH_BLOCK_LAYOUT, EH_FORCE_SEARCH = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 _FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -39,7 +39,7 @@ class EHConfig(ctypes.Structure):
                 ("min_bitset_card", ctypes.c_uint32), ("order", ctypes.c_uint32),
                 ("bin_thread_max", ctypes.c_uint32)]
 
-ORDERS = {"degree": 0, "rev_degree": 1, "random": 2, "bfs": 3, "hybrid": 4, "shingle": 5}
+ORDERS = {"degree": 0, "rev_degree": 1, "random": 2, "bfs": 3, "hybrid": 4, "shingle": 5, "id": 6}
 
 
 class EHStats(ctypes.Structure):
@@ -177,7 +177,7 @@ class Stats:
 class Graph:
     """A loaded trie (eh_graph*).  ``Graph(src, dst, ...)`` == eh_load_edges_ex."""
 
-    def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False,
+    def __init__(self, src, dst, *, tau: int = 0, all_uint: bool = False, no_algo: bool = False, force_search: bool = False,
                  block_layout: bool = False, order: str = "degree", bin_small_max: int = 0,
                  bin_large_min: int = 0, bin_thread_max: int = 0, min_bitset_card: int = 0, stream=None,
                  device: int | None = None,
@@ -193,7 +193,7 @@ class Graph:
         cfg = EHConfig()
         cfg.bitset_tau = tau
         cfg.flags = (EH_INPUT_ON_DEVICE if sdev else 0) | (EH_ALL_UINT if all_uint else 0) | (EH_NO_ALGO if no_algo else 0) \
-            | (EH_BLOCK_LAYOUT if block_layout else 0)
+            | (EH_BLOCK_LAYOUT if block_layout else 0) | (EH_FORCE_SEARCH if force_search else 0)
         if device is not None:
             cfg.flags |= EH_SET_DEVICE
             cfg.device = device

@@ -120,7 +120,7 @@ def test_star_with_path_hub():
     _check(s, d)
 
 
-@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True),
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(force_search=True),
                                 dict(bin_small_max=2**32 - 1), dict(bin_large_min=1), dict(min_bitset_card=1)])
 def test_layout_and_binning_invariance(kw):
     src, dst = synth.rmat(13, 16, 4242)

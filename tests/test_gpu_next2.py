@@ -80,7 +80,7 @@ def test_star_with_path_hub_unstaged():
     assert _gpu(s, d)[0] == 6 * 199_999
 
 
-@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True),
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(force_search=True),
                                 dict(bin_small_max=2**32 - 1), dict(bin_large_min=1), dict(min_bitset_card=1)])
 def test_layout_and_binning_invariance(kw):
     src, dst = synth.rmat(13, 16, 4243)
@@ -169,7 +169,7 @@ def test_k4_pruned_hub_rows():
         assert g.count_4cliques() == comb(1100, 4)
 
 
-@pytest.mark.parametrize("kw", [dict(tau=2), dict(all_uint=True), dict(no_algo=True), dict(bin_large_min=1)])
+@pytest.mark.parametrize("kw", [dict(tau=2), dict(all_uint=True), dict(no_algo=True), dict(force_search=True), dict(bin_large_min=1)])
 def test_k4_unpruned_invariance(kw):
     src, dst = synth.rmat(11, 16, 77)
     assert _k4u(src, dst)[0] == _k4u(src, dst, **kw)[0] == 24 * _k4u(src, dst)[1]

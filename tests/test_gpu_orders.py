@@ -13,7 +13,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-ORDERS = ["degree", "rev_degree", "random", "bfs", "hybrid", "shingle"]
+ORDERS = ["degree", "rev_degree", "random", "bfs", "hybrid", "shingle", "id"]
 
 
 def _edges_from_export(row_ptr, col, orig):
@@ -74,6 +74,17 @@ def test_ordering_edge_cases(order):
     d = np.concatenate([d1, d2 + 1000, np.array([5001], np.uint32)])
     with eh.Graph(s, d, order=order) as g:
         assert g.count_triangles() == 9880 and g.count_4cliques() == 91390
+
+
+def test_id_order_orients_by_input_id():
+    """EH_ORDER_ID: rank = position of the id among the active ids, edges low -> high id."""
+    src, dst = synth.rmat(10, 8, 5)
+    with eh.Graph(src, dst, order="id") as g:
+        row_ptr, col, orig, _ = g.export()
+        assert g.count_triangles() == oracle.count_triangles(src, dst)
+    assert np.all(np.diff(orig.astype(np.int64)) > 0)  # ranks ascend by id
+    act = np.unique(np.concatenate([src[src != dst], dst[src != dst]]))
+    assert np.array_equal(orig, act)
 
 
 def test_unknown_order_is_einval():

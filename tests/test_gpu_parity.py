@@ -211,7 +211,7 @@ def test_block_cache_reuse_across_streams():
 
 
 # ------------------------------------------------------------------ invariances (T5/T6) --
-@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(block_layout=True),
+@pytest.mark.parametrize("kw", [dict(tau=256), dict(tau=2), dict(tau=1 << 20), dict(all_uint=True), dict(no_algo=True), dict(force_search=True), dict(block_layout=True),
                                 dict(block_layout=True, tau=2), dict(block_layout=True, bin_large_min=1),
                                 dict(min_bitset_card=1), dict(bin_small_max=2**32 - 1),
                                 dict(bin_small_max=1, bin_large_min=1), dict(bin_small_max=1, bin_large_min=2**32 - 1),

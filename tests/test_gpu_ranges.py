@@ -227,6 +227,16 @@ def test_count_batch_pipelined_uploads():
     assert eh.count_batch([]) == []
 
 
+def test_count_batch_lanes_with_different_sizes():
+    """Two lanes loading graphs of different id widths at the same time launch the same
+    ingest kernels with different dynamic shared-memory sizes; the per-kernel limit must
+    never drop below what the other lane is about to launch with."""
+    a, b = synth.rmat(8, 8, 4801), synth.rmat(13, 16, 4802)
+    ra, rb = oracle.count_triangles(*a), oracle.count_triangles(*b)
+    for _ in range(25):
+        assert eh.count_batch([a, b, a, b, b, a]) == [ra, rb, ra, rb, rb, ra]
+
+
 def test_count_batch_repeated_calls_release_lane_resources():
     """Every two-lane batch runs one lane on a fresh host thread whose side streams
     are destroyed at its exit: many calls in a row neither leak nor slow down."""

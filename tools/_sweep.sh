@@ -1,5 +1,5 @@
-for c in C3 C4 C2; do
-python tools/load_sweep.py $c EH_TEST_BKT_PART_MATCH - 1
+A=paper_1503_02368_b200/lib/libeh_alt.so
+for c in C3 C4 C2 C5; do
+python tools/tri_sweep.py $c EH_DUMMY - 
+TRI_LIB=$A python tools/tri_sweep.py $c EH_DUMMY_ALT -
 done
-EH_TIMING=1 python tools/profile_load.py --reps 3 2>&1 | grep timing | tail -1
-EH_TIMING=1 python tools/profile_load.py --config C5 --reps 2 2>&1 | grep timing | tail -1
