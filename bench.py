@@ -87,55 +87,124 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML polled every
+    10 ms from a thread of this process (the timed region of the default run is a few
+    hundred ms, shorter than nvidia-smi's start-up); if NVML is unavailable, an
+    `nvidia-smi -lms 100` child started before the warm-up whose lines are kept when they
+    arrive inside the [begin(), stop()] window."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.nvml = None
+        self.handle = None
+        self.samples: list[tuple[float, float, float, int]] = []  # (time, sm, sm_max, reason mask)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.source = None
 
-    def start(self):
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
         except Exception:
-            self.proc = None
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip()]
+            phys = int(ids[self.index]) if ids and all(v.strip().isdigit() for v in ids) else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+        return pynvml, h
+
+    def prepare(self):
+        """Before the warm-up: open NVML (or start the nvidia-smi child)."""
+        try:
+            self.nvml, self.handle = self._nvml_handle()
+            self.nvml.nvmlDeviceGetClockInfo(self.handle, self.nvml.NVML_CLOCK_SM)
+            self.source = "nvml, 10 ms"
+            self.t = threading.Thread(target=self._poll, daemon=True)
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.source = "nvidia-smi -lms 100"
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
+
+    def begin(self):
+        """Start of the timed region."""
+        if self.nvml is None and self.proc is None and self.source is None:
+            self.prepare()
+        self.t0 = time.perf_counter()
+        if self.nvml is not None:
+            self.t.start()
+
+    def _sample_nvml(self):
+        n, h = self.nvml, self.handle
+        sm = float(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM))
+        smax = float(n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM))
+        try:
+            mask = int(n.nvmlDeviceGetCurrentClocksEventReasons(h))
+        except Exception:
+            mask = int(n.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+        self.samples.append((time.perf_counter(), sm, smax, mask))
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                self._sample_nvml()
+            except Exception:
+                break
+            self._stop.wait(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
+            parts = [q.strip() for q in line.split(",")]
             if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
+                sm, smax = float(parts[0]), float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+            mask = 0
+            for (_, bit), v in zip(self.REASONS, parts[4:8]):
                 if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                    mask |= bit
+            self.samples.append((time.perf_counter(), sm, smax, mask))
+
+    def stop(self):
+        self.t1 = time.perf_counter()
+        self._stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
+        elif self.proc is not None:
+            time.sleep(0.12)  # a line in flight for the end of the window
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml and nvidia-smi unavailable"], "samples": 0}
+        tol = 0.0 if self.nvml is not None else 0.1
+        win = [q for q in self.samples if self.t0 - tol <= q[0] <= self.t1 + tol]
+        mask = 0
+        for q in win:
+            mask |= q[3]
+        return {"sm_mhz": statistics.median(q[1] for q in win) if win else None,
+                "sm_max_mhz": max(q[2] for q in win) if win else None,
+                "reasons": sorted(nm for nm, bit in self.REASONS if mask & bit), "samples": len(win),
+                "source": self.source}
 
 
 def _dist():
@@ -297,16 +366,17 @@ def run_gpu(args, cfg, src, dst, n_in):
         stream.synchronize()
         return ev[0].elapsed_time(ev[2]), ev[1].elapsed_time(ev[2]), c, st
 
+    clocks = ClockSampler(local)
+    clocks.prepare()
     # warm-up
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
             _flush_l2(flush)
         one_step(False)
-    clocks = ClockSampler(local)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.begin()
     l0 = eh.launch_count()
     step_ms, count_ms, counts = [], [], set()
     for _ in range(args.steps):

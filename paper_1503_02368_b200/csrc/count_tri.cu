@@ -66,8 +66,11 @@ enum XMode : uint32_t { kBitmap = 0, kHash = 1, kSorted = 2, kHashF = 3 };
 
 // ---------------------------------------------- x's membership structure --
 // N+(x) in shared memory as (a) an exact bitmap over [lo, lo + nbits), (b) an
-// open-addressing hash table with 2^hbits slots (load <= 1/4), or (c) the
-// sorted list itself (binary search; CTA kernel only when |N+(x)| > xcap).
+// open-addressing hash table with 2^hbits slots (load <= 1/2), alone (kHash) or
+// behind a one-hash filter with 32 bits per home slot (kHashF: a miss -- most
+// lookups of a STREAM row -- is one shared-memory load and never walks a probe
+// chain; C5 855 -> 728 ms), or (c) the sorted list itself (binary search; CTA
+// kernel only when |N+(x)| > xcap).
 struct XSet {
   uint32_t* tab;        // bitmap words or hash slots (shared memory)
   const uint32_t* xs;   // sorted N+(x) (shared or global)
@@ -111,7 +114,9 @@ struct XSet {
 };
 
 // Choose the structure (no shared-memory writes): exact bitmap if x's span fits
-// the budget, else a hash with load <= 1/8 (<= 1/4 when the budget is tight).
+// the budget; else, when 4d words fit, a one-hash filter in front of a hash table
+// (kHashF); else a hash with load <= 1/2 (<= 1/8 when the budget allows); else a
+// binary search of the staged list.
 __device__ __forceinline__ XSet plan_xset(uint32_t* tab, uint32_t tab_words, const uint32_t* xs, uint32_t d) {
   XSet s;
   s.tab = tab;
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
                                                             const unsigned long long* __restrict__ items,
                                                             const uint32_t* __restrict__ hslot,
                                                             uint32_t* __restrict__ hub_bm, uint32_t hub_words,
-                                                            BlockView bv) {
+                                                            BlockView bv, uint32_t cslot) {
   // kUnpruned: work items are (x << 32 | first row) over row ranges of kRowsPerItem
   // (hub lists of the symmetric trie would otherwise leave one CTA with 10^5 rows)
   const uint32_t xcap = kXCap > 0 ? (uint32_t)kXCap : xcap_rt;
@@ -643,7 +648,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
     __shared__ uint4 s_dx[2];
     __shared__ unsigned long long s_wi2[2];
     auto prefetch = [&](int b) {  // thread 0
-      const unsigned long long w = atomicAdd(&ctr[2], 1ull);
+      const unsigned long long w = atomicAdd(&ctr[cslot], 1ull);
       s_wi2[b] = w;
       if (w < nwork) {
         const uint4 q = __ldg(desc + __ldg(work + w));
@@ -686,7 +691,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kMinB) k_tri_cta(const uint4* 
     return;
   }
   for (;;) {
-    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[2], 1ull);
+    if (threadIdx.x == 0) s_wi = atomicAdd(&ctr[cslot], 1ull);
     __syncthreads();
     const unsigned long long wi = s_wi;
     if (wi >= nwork) break;
@@ -790,11 +795,16 @@ __global__ void k_hub_fill(const uint4* __restrict__ desc, const uint32_t* __res
 
 template <int NW, int TABW, int XCAP, bool kUnpruned, bool kBlock, int kMinB = 0, int kCG = kG, uint32_t kSF = 64,
           bool kPiv = false>
-void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
+void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap, const uint32_t* work = nullptr,
+                cudaStream_t st = nullptr, uint32_t cslot = 2) {
+  // work / st / cslot: another work list (default: classes 1-2 of g->work after nsmall
+  // entries), stream and work-cursor slot of the count buffer (pruned nests only)
+  if (nlarge == 0) return;
+  if (!work) work = g->work + nsmall;
   if (XCAP > 0) xcap = XCAP;
   auto k = k_tri_cta<NW, TABW, XCAP, kUnpruned, kBlock, kMinB, kCG, kSF, kPiv>;
   const size_t smem = (size_t)((!kUnpruned && !kBlock && NW == 16 ? 2 : 1) * xcap + TABW) * 4;  // TMA: two buffers
-  cudaStream_t s = g->stream;
+  cudaStream_t s = st ? st : g->stream;
   DBuf<unsigned long long> items;
   DBuf<uint32_t> hslot, hubk, hub_bm;
   uint32_t hub_words = 0;
@@ -808,7 +818,7 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
     uint64_t hub_min = xcap, nh = 0;
     for (;;) {
       EH_CUDA(cudaMemsetAsync(hslot.p, 0xFF, nlarge * 4, s));
-      nh = select_if(nlarge, HubPred{g->desc, g->work + nsmall, (uint32_t)std::min<uint64_t>(hub_min, UINT32_MAX)},
+      nh = select_if(nlarge, HubPred{g->desc, work, (uint32_t)std::min<uint64_t>(hub_min, UINT32_MAX)},
                      HubEmit{hslot.p, hubk.p}, g->alloc, s);
       if (nh * hub_words * 4ull <= kHubBitmapBudget || hub_min > g->max_dplus) break;
       hub_min *= 2;
@@ -820,26 +830,26 @@ void launch_cta(eh_graph* g, uint64_t nsmall, uint64_t nlarge, uint32_t xcap) {
     if (nh) {
       hub_bm = DBuf<uint32_t>(g->alloc, nh * hub_words);
       EH_CUDA(cudaMemsetAsync(hub_bm.p, 0, hub_bm.bytes(), s));
-      k_hub_fill<<<(unsigned)nh, 1024, 0, s>>>(g->desc, g->col, g->work + nsmall, hubk.p, hub_words, hub_bm.p);
+      k_hub_fill<<<(unsigned)nh, 1024, 0, s>>>(g->desc, g->col, work, hubk.p, hub_words, hub_bm.p);
       EH_LAUNCH("k_hub_fill");
     }
     DBuf<uint32_t> cnt(g->alloc, nlarge);
     DBuf<uint64_t> off(g->alloc, nlarge + 1), tot(g->alloc, 1);
-    k_item_count<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->desc, g->work + nsmall, nlarge, cnt.p);
+    k_item_count<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->desc, work, nlarge, cnt.p);
     EH_LAUNCH("k_item_count");
     scan_exclusive_u32(cnt.p, off.p, nlarge, tot.p, g->alloc, s);
     nitems = read_scalar(tot.p, s);
     items = DBuf<unsigned long long>(g->alloc, nitems);
-    k_item_emit<<<grid_for(nlarge, 1024), 256, 0, s>>>(g->work + nsmall, nlarge, cnt.p, off.p, items.p);
+    k_item_emit<<<grid_for(nlarge, 1024), 256, 0, s>>>(work, nlarge, cnt.p, off.p, items.p);
     EH_LAUNCH("k_item_emit");
   }
   ensure_dyn_smem((const void*)k, smem);
   int per_sm = 0;
   EH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, smem));
   const unsigned grid = (unsigned)std::min<uint64_t>(nitems, (uint64_t)kSMs * std::max(1, per_sm));
-  k<<<grid, NW * 32, smem, s>>>(g->desc, g->col, g->bs, g->work + nsmall, nitems, g->d_counter, xcap, items.p,
+  k<<<grid, NW * 32, smem, s>>>(g->desc, g->col, g->bs, work, nitems, g->d_counter, xcap, items.p,
                                 kUnpruned ? hslot.p : nullptr, hub_bm.p, hub_words,
-                                BlockView{g->bdesc, g->bcol, g->bcid, g->bmask});
+                                BlockView{g->bdesc, g->bcol, g->bcid, g->bmask}, cslot);
   EH_LAUNCH("k_tri_cta");
   if (kUnpruned) EH_CUDA(cudaStreamSynchronize(s));  // items is released on return
 }
@@ -862,6 +872,29 @@ void launch_warp(eh_graph* g, uint64_t nsmall, const uint32_t* work = nullptr, u
                                                BlockView{g->bdesc, g->bcol, g->bcid, g->bmask}, cslot);
   EH_LAUNCH("k_tri_warp");
 }
+
+#ifndef EH_MID_NW
+#define EH_MID_NW 4
+#endif
+#ifndef EH_MID_CG
+#define EH_MID_CG kG
+#endif
+#ifndef EH_MID_TABW
+#define EH_MID_TABW 2048
+#endif
+// wide shape: class-2 x with |N+(x)| <= kMidMax (0 / 1 of the 2-way split)
+constexpr uint32_t kMidMax = 512;  // the 4-warp CTA's 2048-word table holds filter + hash up to 512 elements
+struct MidClass {
+  const uint4* desc;
+  const uint32_t* w;
+  uint32_t mid;
+  __device__ int operator()(uint64_t i) const { return desc[w[i]].y <= mid ? 0 : 1; }
+};
+struct MidEmit {
+  const uint32_t* w;
+  uint32_t* out;
+  __device__ void operator()(int, uint64_t pos, uint64_t i) const { out[pos] = w[i]; }
+};
 
 template <bool kUnpruned, bool kBlock>
 uint64_t count_impl(eh_graph* g) {
@@ -902,6 +935,10 @@ uint64_t count_impl(eh_graph* g) {
       launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, nsmall - g->n_work[0], g->work + g->n_work[0], 6u, ss);
     } else launch_warp<kUnpruned, kBlock, kWarpMaxD, 0, kG, 64, true>(g, n0, w0, 1u, ss);
   }
+  DBuf<uint32_t> split;  // wide shape: class 2 as (mid x, big x)
+  // test hook EH_TEST_TRI_MID: the mid / big boundary (0 = no mid class)
+  uint32_t mid_max = kMidMax;
+  if (const char* e = getenv("EH_TEST_TRI_MID")) mid_max = (uint32_t)atoi(e);
   if (nlarge) {
     // unpruned: lists above 4096 use the global hub bitmaps (measured: C3 0.93 -> 0.42 s)
     const uint64_t cap = kUnpruned ? 4096 : wide ? kCtaXCapMax : kCtaXCapNarrow;
@@ -911,8 +948,28 @@ uint64_t count_impl(eh_graph* g) {
     // follows the graph size (L2-resident lists: C3 unpruned 415.6 -> 386.9 ms)
     if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096)
       launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, 0);
-    else if (wide && xcap <= 4096 && !getenv("EH_TEST_TRI_XCAP"))
-      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, 0);
+    else if (wide && xcap <= 4096 && !getenv("EH_TEST_TRI_XCAP")) {
+      // Wide shape, pruned set-level nest: the x with |N+(x)| <= kMidMax take the 4-warp
+      // CTAs (8 KB table: one-hash filter + hash table, many CTAs per SM, so the per-x
+      // barrier tails overlap), the rest the 16-warp CTAs with the 64 KB table.  The class
+      // list is split per call (one stable 2-way partition of its entries).
+      uint64_t nmid = 0;
+      if (!kUnpruned && !kBlock && mid_max >= tri_warp_max_degree() + 1) {
+        split = DBuf<uint32_t>(g->alloc, nlarge);
+        uint64_t st2[3];
+        partition_k<2>(nlarge, MidClass{g->desc, g->work + nsmall, mid_max}, MidEmit{g->work + nsmall, split.p}, st2,
+                       g->alloc, s);
+        nmid = st2[1] - st2[0];
+      }
+      const uint32_t* wbig = nmid ? split.p + nmid : nullptr;
+      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge - nmid, 0, wbig);
+      if (nmid) {
+        const cudaStream_t sm = (nlarge > nmid && getenv("EH_TEST_TRI_SERIAL") == nullptr) ? fork_side(g, 1) : s;
+        launch_cta<EH_MID_NW, EH_MID_TABW, 0, kUnpruned, kBlock, 0, EH_MID_CG, 64, true>(g, nsmall, nmid, (mid_max + 255) / 256 * 256, split.p, sm,
+                                                                   3u);
+        if (sm != s) join_side(g, 1);
+      }
+    }
     else if (wide) launch_cta<16, 16384, 0, kUnpruned, kBlock, 0, kG, 64, true>(g, nsmall, nlarge, xcap);
     // rows on 4-lane groups (32 rows in flight per CTA) below 2^20 active ids, 8-lane
     // groups above (measured: C2 0.348 -> 0.325, C4 1.556 -> 1.508, C3 9.42 -> 9.46 ms)

@@ -177,6 +177,28 @@ def test_wide_shape_tma_staging(monkeypatch, xcap):
         assert g.count_triangles() == ref
 
 
+@pytest.mark.parametrize("mid", ["0", "135", "512", "4096"])
+def test_wide_shape_mid_class(monkeypatch, mid):
+    # wide shape: class-2 x with |N+(x)| <= EH_TEST_TRI_MID (default 512) run on 4-warp CTAs
+    # beside the 16-warp CTAs of the rest; any boundary (none, both classes populated, all
+    # mid) gives the oracle's count, and the rank-range counts still add up
+    from math import comb
+    src, dst = synth.rmat(14, 16, 41)
+    ref = oracle.count_triangles(src, dst)
+    monkeypatch.setenv("EH_TEST_TRI_WIDE", "1")
+    monkeypatch.setenv("EH_TEST_TRI_MID", mid)
+    with eh.Graph(src, dst) as g:
+        st = g.stats()
+        assert st.max_out_degree > 135
+        assert g.count_triangles() == ref
+        cut = st.n_active - 3000
+        assert g.count_triangles_range(0, cut) + g.count_triangles_range(cut, st.n_active) == ref
+    n = 700  # K_700: |N+(x)| = 699 .. 0, both classes at the default boundary
+    iu = np.triu_indices(n, 1)
+    with eh.Graph(iu[0].astype(np.uint32), iu[1].astype(np.uint32)) as g:
+        assert g.count_triangles() == comb(n, 3)
+
+
 @pytest.mark.parametrize("offset", [0, 1, 3])
 def test_device_inputs_unaligned(offset):
     # device-resident inputs that start 4 / 12 bytes past an aligned address: the

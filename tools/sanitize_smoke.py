@@ -58,6 +58,15 @@ with eh.Graph(src, dst, block_layout=True, order="bfs", bin_thread_max=16) as g:
 os.environ["EH_TEST_TRI_WIDE"] = "1"
 with eh.Graph(src, dst) as g:
     assert g.count_triangles() == T
+ws, wd = synth.rmat(14, 16, 41)  # max |N+(x)| = 145: the wide shape's CTA classes
+wT = oracle.count_triangles(ws, wd)
+with eh.Graph(ws, wd) as g:
+    assert g.count_triangles() == wT   # all of class 2 on the 4-warp (mid) CTAs
+    os.environ["EH_TEST_TRI_MID"] = "135"  # mid and big (16-warp, TMA-staged) CTA classes both populated
+    assert g.count_triangles() == wT
+    os.environ["EH_TEST_TRI_MID"] = "0"  # all of class 2 on the 16-warp CTAs
+    assert g.count_triangles() == wT
+    del os.environ["EH_TEST_TRI_MID"]
 del os.environ["EH_TEST_TRI_WIDE"]
 assert eh.count_batch([(src, dst), (src[:1000], dst[:1000]), (src, dst)])[0] == T
 og.close()
