@@ -57,6 +57,10 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   return x;
 }
 
+// row pitch of the per-(chunk, CTA) histograms: one 128-B line past the power of two (rows at
+// exactly 64 KB apart made k_bkt_colscan's strided reads 4.6x slower: 437 vs 95 us at C3)
+__host__ __device__ __forceinline__ uint64_t pitch(uint32_t nb) { return (uint64_t)nb + 32; }
+
 // pair -> (bucket, residual); false for a self-loop (dropped, reading c5)
 __device__ __forceinline__ bool pair_bucket(uint32_t u, uint32_t v, const BktParams& p, uint32_t& bk, uint32_t& r) {
   if (u == v) return false;
@@ -66,57 +70,157 @@ __device__ __forceinline__ bool pair_bucket(uint32_t u, uint32_t v, const BktPar
   return true;
 }
 
+// f(u, v, ok) over the pairs [p0, p1) (p0 a multiple of 4), grid-stride, 128-bit loads when
+// the inputs are 16-B aligned; every lane of a warp runs the same number of rounds (f may use
+// warp collectives)
 template <class F>
-__device__ __forceinline__ void for_pairs(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
-                                          uint64_t n, F f) {
+__device__ __forceinline__ void for_pairs_range(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                                uint64_t p0, uint64_t p1, F f) {
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t done = 0;
+  uint64_t done = p0;
   if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {  // 128-bit loads
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     const uint4* d4 = reinterpret_cast<const uint4*>(dst);
-    const uint64_t n4 = n / 4;
-    // every lane of a warp runs the same number of rounds (f may use warp collectives)
-    for (uint64_t i0 = t0 - (threadIdx.x & 31); i0 < n4; i0 += nt) {
-      const uint64_t i = i0 + (threadIdx.x & 31);
-      const bool ok = i < n4;
-      const uint4 a = ok ? __ldcs(s4 + i) : make_uint4(0, 0, 0, 0), c = ok ? __ldcs(d4 + i) : make_uint4(0, 0, 0, 0);
+    const uint64_t v1 = p1 / 4;
+    // the next round's loads are issued before this round's pairs are processed
+    uint64_t i = p0 / 4 + t0;
+    bool ok = i < v1;
+    uint4 a = ok ? __ldcs(s4 + i) : make_uint4(0, 0, 0, 0), c = ok ? __ldcs(d4 + i) : make_uint4(0, 0, 0, 0);
+    for (uint64_t i0 = p0 / 4 + t0 - (threadIdx.x & 31); i0 < v1; i0 += nt) {
+      const uint64_t in = i + nt;
+      const bool okn = in < v1;
+      const uint4 an = okn ? __ldcs(s4 + in) : make_uint4(0, 0, 0, 0), cn = okn ? __ldcs(d4 + in) : make_uint4(0, 0, 0, 0);
       f(a.x, c.x, ok); f(a.y, c.y, ok); f(a.z, c.z, ok); f(a.w, c.w, ok);
+      i = in; ok = okn; a = an; c = cn;
     }
-    done = n4 * 4;
+    done = v1 * 4;
   }
-  for (uint64_t i0 = done + t0 - (threadIdx.x & 31); i0 < n; i0 += nt) {
+  for (uint64_t i0 = done + t0 - (threadIdx.x & 31); i0 < p1; i0 += nt) {
     const uint64_t i = i0 + (threadIdx.x & 31);
-    const bool ok = i < n;
+    const bool ok = i < p1;
     f(ok ? src[i] : 0u, ok ? dst[i] : 0u, ok);
   }
 }
+template <class F>
+__device__ __forceinline__ void for_pairs(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                          uint64_t n, F f) {
+  for_pairs_range(src, dst, 0, n, f);
+}
 
-// (1) bucket histogram; kSmem: per-CTA shared-memory counters, else warp-aggregated global atomics
+// (1) bucket histogram; kSmem: per-CTA shared-memory counters, else warp-aggregated global atomics.
+// percta (kSmem only): the input is taken in chunks of `per` pairs and this CTA's own
+// histogram of chunk c goes to percta[(c * gridDim.x + blockIdx.x) * nb + .] instead of cnt
+// (k_bkt_colscan sums them and turns the entries into the cursors of k_bkt_part_smem).
 template <bool kSmem>
 __global__ void __launch_bounds__(1024) k_bkt_hist(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
-                                                  uint64_t n, BktParams p, uint32_t nb, uint32_t* __restrict__ cnt) {
+                                                  uint64_t n, BktParams p, uint32_t nb, uint32_t* __restrict__ cnt,
+                                                  uint32_t* __restrict__ percta, uint64_t per) {
   extern __shared__ uint32_t sh_hist[];
-  if (kSmem) {
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh_hist[i] = 0;
-    __syncthreads();
-  }
   const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
-  for_pairs(src, dst, n, [&](uint32_t u, uint32_t v, bool ok) {
-    uint32_t bk = 0xFFFFFFFFu, r;
-    if (!(ok && pair_bucket(u, v, p, bk, r))) bk = 0xFFFFFFFFu;
+  if (!percta) per = n;
+  uint32_t chunk = 0;
+  for (uint64_t p0 = 0; p0 < n || p0 == 0; p0 += per, ++chunk) {
     if (kSmem) {
-      if (bk != 0xFFFFFFFFu) atomicAdd(&sh_hist[bk], 1u);
-    } else {
-      const unsigned peers = __match_any_sync(kFull, bk);
-      if (bk != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&cnt[bk], (uint32_t)__popc(peers));
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh_hist[i] = 0;
+      __syncthreads();
     }
-  });
-  if (kSmem) {
+    for_pairs_range(src, dst, p0, min(n, p0 + per), [&](uint32_t u, uint32_t v, bool ok) {
+      uint32_t bk = 0xFFFFFFFFu, r;
+      if (!(ok && pair_bucket(u, v, p, bk, r))) bk = 0xFFFFFFFFu;
+      if (kSmem) {
+        if (bk != 0xFFFFFFFFu) atomicAdd(&sh_hist[bk], 1u);
+      } else {
+        const unsigned peers = __match_any_sync(kFull, bk);
+        if (bk != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&cnt[bk], (uint32_t)__popc(peers));
+      }
+    });
+    if (kSmem) {
+      __syncthreads();
+      uint32_t* mine = percta ? percta + ((uint64_t)chunk * gridDim.x + blockIdx.x) * pitch(nb) : nullptr;
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+        const uint32_t c = sh_hist[i];
+        if (mine) mine[i] = c;
+        else if (c) atomicAdd(&cnt[i], c);
+      }
+      __syncthreads();
+    }
+    if (per == 0) break;
+  }
+}
+
+// (2') per-(chunk, CTA) histograms -> exclusive offsets inside each bucket (in part order),
+// and the bucket totals.  One CTA per kCsB buckets: thread (bx, seg) owns a contiguous segment
+// of the parts of bucket blockIdx.x * kCsB + bx (loads coalesced over bx, independent over
+// the segment), the kCsS segment sums are scanned in shared memory, a second pass writes the
+// offsets.  (64 segments of 16 buckets: with 32 x 32 the 84 dependent rounds per thread of a
+// 2664-part scan took 437 us at C3 with 2^14 buckets.)
+constexpr uint32_t kCsB = 16, kCsS = 64;
+__global__ void __launch_bounds__(kCsB * kCsS) k_bkt_colscan(uint32_t* __restrict__ percta, uint32_t nparts, uint32_t nb,
+                                                            uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t seg_sum[kCsS][kCsB + 1];
+  const uint32_t bx = threadIdx.x % kCsB, seg = threadIdx.x / kCsB;
+  const uint32_t b = blockIdx.x * kCsB + bx;
+  const uint32_t per = (nparts + kCsS - 1) / kCsS;
+  const uint64_t ld = pitch(nb);
+  const uint32_t c0 = min(nparts, seg * per), c1 = min(nparts, c0 + per);
+  uint32_t sum = 0;
+  if (b < nb) {
+#pragma unroll 8
+    for (uint32_t c = c0; c < c1; ++c) sum += percta[(uint64_t)c * ld + b];
+  }
+  seg_sum[seg][bx] = sum;
+  __syncthreads();
+  if (seg == 0) {  // lane bx scans the segment sums of its bucket
+    uint32_t run = 0;
+    for (uint32_t q = 0; q < kCsS; ++q) {
+      const uint32_t v = seg_sum[q][bx];
+      seg_sum[q][bx] = run;
+      run += v;
+    }
+    if (b < nb) cnt[b] = run;
+  }
+  __syncthreads();
+  if (b < nb) {
+    uint32_t run = seg_sum[seg][bx];
+#pragma unroll 8
+    for (uint32_t c = c0; c < c1; ++c) {
+      const uint32_t v = percta[(uint64_t)c * ld + b];
+      percta[(uint64_t)c * ld + b] = run;
+      run += v;
+    }
+  }
+}
+
+// (3'') residuals into their buckets without global atomics: the same grid, chunks and pair
+// assignment as k_bkt_hist<true>, whose per-(chunk, CTA) counts (k_bkt_colscan) give every
+// CTA its own range inside each bucket for each chunk; the cursors live in shared memory.
+// (The global cursor atomics of k_bkt_part_direct ran at ~60 G atomics/s, 69 % of its stall
+// samples waiting on their results: C3 1.16 ms for 0.8 GB of traffic.)  A bucket's range is
+// laid out chunk-major, so the sectors written during one chunk (all CTAs advance through
+// the chunks together) add up to the chunk's own output -- sized to stay in L2 until the
+// sectors are complete (unchunked, C3's 4.8 M runs of ~14 entries were evicted half-written:
+// 1.97 ms).
+__global__ void __launch_bounds__(1024) k_bkt_part_smem(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                                       uint64_t n, BktParams p, uint32_t nb,
+                                                       const uint64_t* __restrict__ boff,
+                                                       const uint32_t* __restrict__ percta, uint64_t per,
+                                                       uint32_t* __restrict__ part) {
+  extern __shared__ uint32_t sh_cur[];
+  uint32_t chunk = 0;
+  for (uint64_t p0 = 0; p0 < n; p0 += per, ++chunk) {
+    const uint32_t* mine = percta + ((uint64_t)chunk * gridDim.x + blockIdx.x) * pitch(nb);
+#pragma unroll 8
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) sh_cur[i] = (uint32_t)boff[i] + mine[i];
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-      const uint32_t c = sh_hist[i];
-      if (c) atomicAdd(&cnt[i], c);
-    }
+    for_pairs_range(src, dst, p0, min(n, p0 + per), [&](uint32_t u, uint32_t v, bool ok) {
+      uint32_t bk, r;
+      if (ok && pair_bucket(u, v, p, bk, r)) {
+        const uint32_t q = atomicAdd(&sh_cur[bk], 1u);
+        EH_DASSERT(q >= boff[bk] && q < boff[bk + 1]);
+        part[q] = r;
+      }
+    });
+    __syncthreads();
   }
 }
 
@@ -319,9 +423,23 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
                   unsigned long long* m_ctr, uint64_t* out, eh_graph* g, PhaseTimer* tm) {
   Allocator& al = g->alloc;
   cudaStream_t s = g->stream;
-  // bb bucket bits: residual <= 31 bits, <= 2^12 lo values per bucket, ~4096 pairs per bucket
+  // bb bucket bits: residual <= 31 bits, <= 2^12 lo values per bucket, 4096 - 8192 pairs per bucket
+  // on average (measured with the shared-memory partition, EH_TEST_BKT_SHIFT -2 / -1 / 0 / 1 around
+  // n >> 12: C3 4.89 / 5.00 / 5.10 / -, C4 1.54 / 1.45 / 1.47 / 1.58, C2 0.670 / 0.676 / 0.688 / 0.710 ms)
   int bb = std::max<int>(2 * (int)b - 31, (int)b - kMaxLoBits);
-  bb = std::max<int>(bb, (int)bitlen(n >> 12));
+  bb = std::max<int>(bb, (int)bitlen(n >> 13));
+  // chunks of `per` pairs (a multiple of 4) whose residuals (4 B each) fit 32 MB of L2 (test hook
+  // EH_TEST_BKT_CHUNK_MB; measured at C3, 8 / 16 / 32 / 64 MB / one chunk: load 8.61 / 5.81 / 5.08 /
+  // 5.07 / 5.94 ms)
+  uint64_t chunk_mb = 32;
+  if (const char* e = getenv("EH_TEST_BKT_CHUNK_MB")) chunk_mb = std::max(1, atoi(e));
+  const uint64_t nchunks = std::max<uint64_t>(1, (n * 4 + (chunk_mb << 20) - 1) / (chunk_mb << 20));
+  const uint64_t per = ((n + nchunks - 1) / nchunks + 3) / 4 * 4;
+  // the per-(chunk, CTA) histograms are read twice by the column scan: keep them L2-sized
+  // (C3: 2^14 buckets 175 MB, scan 0.40 ms; 2^13 buckets 87 MB, 0.10 ms)
+  while (bb > std::max<int>(2 * (int)b - 31, (int)b - kMaxLoBits) && bb <= kHistSmemBits &&
+         ((n + per - 1) / per) * (2ull * kSMs) * (4ull << bb) > (96ull << 20))
+    --bb;
   if (const char* e = getenv("EH_TEST_BKT_SHIFT")) bb = std::max<int>(2 * (int)b - 31, bb + atoi(e));  // test hook
   bb = std::max(0, std::min<int>(bb, (int)b));
   const BktParams p{b, b - (uint32_t)bb};
@@ -331,22 +449,41 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   EH_CUDA(cudaMemsetAsync(cur.p, 0, nb * 4ull, s));
   const unsigned TB = 256;
   const unsigned grid_stream = grid_for((n + 3) / 4, TB, kSMs * 8);
-  if (bb <= kHistSmemBits && getenv("EH_TEST_BKT_GHIST") == nullptr) {
-    const size_t sm = nb * 4ull;
+  // shared-memory histogram / cursors (<= 2^15 buckets): 1024-thread CTAs, as many per SM as the
+  // counters allow (one at 2^15 buckets); test hooks: EH_TEST_BKT_GHIST global-atomic histogram,
+  // EH_TEST_BKT_PART_ATOMIC global cursor atomics (both for > 2^15 buckets anyway),
+  // EH_TEST_BKT_PART_MATCH the warp-matched variant of the latter
+  const bool smem_hist = bb <= kHistSmemBits && getenv("EH_TEST_BKT_GHIST") == nullptr;
+  const bool smem_part = smem_hist && n < (1ull << 32) && getenv("EH_TEST_BKT_PART_ATOMIC") == nullptr &&
+                         getenv("EH_TEST_BKT_PART_MATCH") == nullptr;
+  const size_t sm = nb * 4ull;
+  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / std::max<size_t>(sm, 1)));
+  const unsigned grid_sm = std::min(grid_for((n + 3) / 4, 1024), kSMs * per_sm);
+  const uint64_t nparts = (n + per - 1) / per * grid_sm;  // (chunk, CTA) histograms
+  DBuf<uint32_t> percta;
+  if (smem_part) percta = DBuf<uint32_t>(al, nparts * pitch(nb));
+  if (smem_hist) {
     ensure_dyn_smem((const void*)k_bkt_hist<true>, sm);
-    // 1024-thread CTAs, as many per SM as the counters allow (one at 2^15 buckets)
-    const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / std::max<size_t>(sm, 1)));
-    k_bkt_hist<true><<<std::min(grid_for((n + 3) / 4, 1024), kSMs * per_sm), 1024, sm, s>>>(src, dst, n, p, nb, cnt.p);
+    prefer_max_smem_carveout((const void*)k_bkt_hist<true>);
+    k_bkt_hist<true><<<grid_sm, 1024, sm, s>>>(src, dst, n, p, nb, cnt.p, smem_part ? percta.p : nullptr, per);
   } else {
-    k_bkt_hist<false><<<grid_stream, TB, 0, s>>>(src, dst, n, p, nb, cnt.p);
+    k_bkt_hist<false><<<grid_stream, TB, 0, s>>>(src, dst, n, p, nb, cnt.p, nullptr, n);
   }
   EH_LAUNCH("k_bkt_hist");
+  if (smem_part) {
+    k_bkt_colscan<<<(nb + kCsB - 1) / kCsB, kCsB * kCsS, 0, s>>>(percta.p, (uint32_t)nparts, nb, cnt.p);
+    EH_LAUNCH("k_bkt_colscan");
+  }
   DBuf<uint64_t> boff(al, nb + 1ull), tot(al, 1);
   scan_exclusive_u32(cnt.p, boff.p, nb, tot.p, al, s);
   EH_CUDA(cudaMemcpyAsync(boff.p + nb, tot.p, 8, cudaMemcpyDeviceToDevice, s));
   DBuf<uint32_t> part(al, n);
   if (tm) tm->mark("bkt_hist");
-  if (getenv("EH_TEST_BKT_PART_MATCH") == nullptr) {
+  if (smem_part) {
+    ensure_dyn_smem((const void*)k_bkt_part_smem, sm);
+    prefer_max_smem_carveout((const void*)k_bkt_part_smem);
+    k_bkt_part_smem<<<grid_sm, 1024, sm, s>>>(src, dst, n, p, nb, boff.p, percta.p, per, part.p);
+  } else if (getenv("EH_TEST_BKT_PART_MATCH") == nullptr) {
     k_bkt_cursors<<<grid_for(nb, TB), TB, 0, s>>>(boff.p, nb, cur.p);
     EH_LAUNCH("k_bkt_cursors");
     k_bkt_part_direct<<<grid_stream, TB, 0, s>>>(src, dst, n, p, boff.p, cur.p, part.p);
@@ -354,6 +491,7 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
     k_bkt_part<<<grid_stream, TB, 0, s>>>(src, dst, n, p, boff.p, cur.p, part.p);
   }
   EH_LAUNCH("k_bkt_part");
+  percta.reset();
   if (tm) tm->mark("bkt_part");
   cur.reset();
   DBuf<uint32_t> lists(al, 3ull * nb);

@@ -14,6 +14,18 @@
 namespace eh {
 std::atomic<unsigned long long> g_launches{0};
 
+void prefer_max_smem_carveout(const void* kernel) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  EH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  bool& d = done[{dev, kernel}];
+  if (d) return;
+  EH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  d = true;
+}
+
 void ensure_dyn_smem(const void* kernel, size_t bytes) {
   if (bytes <= 48 * 1024) return;  // within the default limit
   static std::mutex mu;

@@ -55,6 +55,10 @@ extern std::atomic<unsigned long long> g_launches;
 // The limit only ever grows (per device and kernel): two host threads launching the same
 // kernel with different sizes (eh_count_batch's lanes) cannot lower it under each other.
 void ensure_dyn_smem(const void* kernel, size_t bytes);
+// Asks for the largest shared-memory carveout for a kernel whose residency is bounded by
+// shared memory (the default heuristic sized the carveout for ONE 32 KB CTA of the bucket
+// histogram / partition kernels: `launch__occupancy_limit_shared_mem` 1 instead of 2).
+void prefer_max_smem_carveout(const void* kernel);
 
 // Device allocator: the caller's hooks (e.g. torch's caching allocator) or cudaMallocAsync.
 // Default device allocation path (no allocator hook): cudaMallocAsync on the

@@ -279,6 +279,30 @@ def test_bucket_classes_with_duplicates(seed):
     _check(s[perm], d[perm])
 
 
+@pytest.mark.parametrize("env", [dict(EH_TEST_BKT_CHUNK_MB="1"), dict(EH_TEST_BKT_PART_ATOMIC="1"),
+                                 dict(EH_TEST_BKT_PART_MATCH="1"), dict(EH_TEST_BKT_GHIST="1"),
+                                 dict(EH_TEST_BKT_SHIFT="2"), dict(EH_TEST_BKT_SHIFT="-3", EH_TEST_BKT_CHUNK_MB="1")])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_bucket_partition_variants(env, offset, monkeypatch):
+    """The bucket partition of dedup.cu: cursors in shared memory from per-(chunk, CTA)
+    histograms (default; EH_TEST_BKT_CHUNK_MB=1 makes several chunks, with ragged last chunk),
+    global cursor atomics (plain / warp-matched), the global-atomic histogram, other bucket
+    widths; 16-B aligned and unaligned device inputs (128-bit / scalar loads).  Same trie."""
+    import torch
+    src, dst = synth.rmat(16, 16, 8800)
+    src, dst = src[:-3], dst[:-3]  # n % 4 != 0
+    ref = (oracle.count_triangles(src[offset:], dst[offset:]), oracle.count_4cliques(src[offset:], dst[offset:]))
+    ts = torch.from_numpy(src.view(np.int32)).cuda()[offset:]
+    td = torch.from_numpy(dst.view(np.int32)).cuda()[offset:]
+    with eh.Graph(ts, td) as g:
+        base = (g.count_triangles(), g.count_4cliques(), g.stats().m_undirected)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with eh.Graph(ts, td) as g:
+        alt = (g.count_triangles(), g.count_4cliques(), g.stats().m_undirected)
+    assert base == alt and base[:2] == ref
+
+
 def test_device_input_and_stream():
     import torch
     src, dst = synth.rmat(12, 16, 6)

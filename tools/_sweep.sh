@@ -1,6 +1,11 @@
-P=paper_1503_02368_b200/lib
-python tools/tri_sweep.py C5 EH_DUMMY -
-for v in cg4 nw8 nw8cg4 tab4096 nw2; do
-TRI_LIB=$P/libeh_$v.so python tools/tri_sweep.py C5 EH_DUMMY_$v -
-done
-python tools/tri_sweep.py C5 EH_DUMMY -
+EH_TIMING=1 python bench.py --steps 8 --warmup 3 --no-cpu-baseline 2>&1 | grep -E "eh timing|^\{" | tail -2 | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print({k:round(d[k],3) for k in ['ms_per_step','count_ms','load_ms']})
+    else: print(l.strip()[100:230])
+"
+python tools/load_sweep.py C4 EH_TEST_BKT_SHIFT -1 0
+python tools/load_sweep.py C2 EH_TEST_BKT_SHIFT -1 0
+python tools/load_sweep.py C5 EH_TEST_BKT_SHIFT 0
+python -m pytest tests -m gpu -x -q -k "bucket or dedup or batch or ingest" 2>&1 | tail -2
