@@ -437,8 +437,12 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   const uint64_t per = ((n + nchunks - 1) / nchunks + 3) / 4 * 4;
   // the per-(chunk, CTA) histograms are read twice by the column scan: keep them L2-sized
   // (C3: 2^14 buckets 175 MB, scan 0.40 ms; 2^13 buckets 87 MB, 0.10 ms)
+  // -- first one CTA per SM instead of two (the partition is no faster with two), then fewer buckets
+  unsigned cta_per_sm = 2;
+  auto hist_bytes = [&](int bits, unsigned k) { return ((n + per - 1) / per) * ((uint64_t)k * kSMs) * (4ull << bits); };
+  if (bb <= kHistSmemBits && hist_bytes(bb, 2) > (96ull << 20)) cta_per_sm = 1;
   while (bb > std::max<int>(2 * (int)b - 31, (int)b - kMaxLoBits) && bb <= kHistSmemBits &&
-         ((n + per - 1) / per) * (2ull * kSMs) * (4ull << bb) > (96ull << 20))
+         hist_bytes(bb, cta_per_sm) > (96ull << 20))
     --bb;
   if (const char* e = getenv("EH_TEST_BKT_SHIFT")) bb = std::max<int>(2 * (int)b - 31, bb + atoi(e));  // test hook
   bb = std::max(0, std::min<int>(bb, (int)b));
@@ -457,7 +461,7 @@ void bucket_dedup(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t
   const bool smem_part = smem_hist && n < (1ull << 32) && getenv("EH_TEST_BKT_PART_ATOMIC") == nullptr &&
                          getenv("EH_TEST_BKT_PART_MATCH") == nullptr;
   const size_t sm = nb * 4ull;
-  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / std::max<size_t>(sm, 1)));
+  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(cta_per_sm, (200 * 1024) / std::max<size_t>(sm, 1)));
   const unsigned grid_sm = std::min(grid_for((n + 3) / 4, 1024), kSMs * per_sm);
   const uint64_t nparts = (n + per - 1) / per * grid_sm;  // (chunk, CTA) histograms
   DBuf<uint32_t> percta;
