@@ -151,12 +151,14 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, uint32_t key
 uint64_t* radix_sort_canon(const uint32_t* src, const uint32_t* dst, uint64_t n, uint32_t b, uint64_t* keys,
                            uint64_t* alt, Allocator& al, cudaStream_t s);
 // Sort segment v = data[off16[v]*4 .. + len[v]) in place for v < nseg (segsort.cu).
+// fork: a handle whose side streams the independent tier kernels may use (nullptr: one stream).
 void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
-                        Allocator& al, cudaStream_t s);
+                        Allocator& al, cudaStream_t s, eh_graph* fork = nullptr);
 // Out of place: segment v = in[ioff[v] .. + len[v]) sorted into out[off16[v]*4 ..) (segments of one
 // element are copied; pads between output segments are left untouched).
 void segmented_sort_u32_into(const uint32_t* in, const uint64_t* ioff, uint32_t* out, const uint64_t* off16,
-                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s);
+                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s,
+                             eh_graph* fork = nullptr);
 // Same for u32 keys.
 uint32_t* radix_sort_u32(uint32_t* keys, uint32_t* alt, uint64_t n, uint32_t key_bits, Allocator& al,
                          cudaStream_t s);

@@ -553,7 +553,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   g->col = (uint32_t*)g->own(std::max<uint64_t>(16, total16 * 16));
   EH_CUDA(cudaMemsetAsync(g->col, 0xFF, std::max<uint64_t>(16, total16 * 16), s));
   mark("orient");
-  segmented_sort_u32_into(tmp.p, toff.p, g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s);
+  segmented_sort_u32_into(tmp.p, toff.p, g->col, off16.p, dplus.p, n_act, (uint32_t)g->max_dplus, al, s, g);
   mark("segsort");
   g->desc = (uint4*)g->own((n_act + 1) * sizeof(uint4));
   k_desc_base<<<grid_for(n_act + 1, TB * 4), TB, 0, s>>>(off16.p, dplus.p, n_act, total16, g->desc);

@@ -245,7 +245,7 @@ __global__ void k_gather_len(const uint32_t* __restrict__ len, const uint32_t* _
 }  // namespace
 
 static void segsort_impl(uint32_t* data, const Seg& sg, uint64_t nseg, uint32_t max_len, Allocator& al,
-                         cudaStream_t s) {
+                         cudaStream_t s, eh_graph* fork) {
   const uint32_t* len = sg.len;
   DBuf<uint32_t> all_ids(al, nseg);
   DBuf<uint64_t> starts(al, 10);  // one partition of the segments by tier, kept on the device:
@@ -253,19 +253,37 @@ static void segsort_impl(uint32_t* data, const Seg& sg, uint64_t nseg, uint32_t 
   // the tier kernels read their range from `starts`; grids are sized for the worst
   // case the host knows (nseg, max_len) and stride over what is there
   const uint32_t tier_min[8] = {1, 33, 65, 129, 257, 513, (uint32_t)kMidMax + 1, (uint32_t)kBigMax + 1};
+  // The tiers are independent (disjoint segments) and each kernel is short and latency-bound
+  // (ids -> length / offset -> keys), so with a handle to fork from they alternate over the
+  // handle's stream and two of its side streams (C3: 0.59 -> see DESIGN.md §6 "ingest").
+  cudaStream_t st[3] = {s, s, s};
+  int ntier = 0;
+  for (int tier = 0; tier < 7 && max_len >= tier_min[tier]; ++tier) ++ntier;
+  const bool forked = fork && ntier >= 2 && getenv("EH_TEST_SEG_SERIAL") == nullptr;
+  if (forked) {
+    st[1] = fork_side(fork, 1);
+    if (ntier >= 3) st[2] = fork_side(fork, 2);
+  }
+  // heaviest first on each stream: tier 0 (all lists <= 32) alone on the handle's stream's head
+  const int lane_of[7] = {0, 1, 2, 1, 2, 1, 2};
   for (int tier = 0; tier < 7; ++tier) {
     if (max_len < tier_min[tier]) break;
     const uint64_t* rng = starts.p + tier;
     const uint64_t kmax = std::min<uint64_t>(nseg, 1ull << 24);
     const unsigned g = grid_for(kmax * 32, 256);
-    if (tier == 0) k_seg_small<<<grid_for(kmax * 8, 256), 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else if (tier == 1) k_seg_regs<2><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else if (tier == 2) k_seg_regs<4><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else if (tier == 3) k_seg_regs<8><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else if (tier == 4) k_seg_regs<16><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else if (tier == 5) k_seg_regs<32><<<g, 256, 0, s>>>(data, sg, all_ids.p, rng);
-    else k_seg_big<<<(unsigned)kSMs * 2, kBigThreads, 0, s>>>(data, sg, all_ids.p, rng);
+    const cudaStream_t ts = st[lane_of[tier]];
+    if (tier == 0) k_seg_small<<<grid_for(kmax * 8, 256), 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else if (tier == 1) k_seg_regs<2><<<g, 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else if (tier == 2) k_seg_regs<4><<<g, 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else if (tier == 3) k_seg_regs<8><<<g, 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else if (tier == 4) k_seg_regs<16><<<g, 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else if (tier == 5) k_seg_regs<32><<<g, 256, 0, ts>>>(data, sg, all_ids.p, rng);
+    else k_seg_big<<<(unsigned)kSMs * 2, kBigThreads, 0, ts>>>(data, sg, all_ids.p, rng);
     EH_LAUNCH(tier == 6 ? "k_seg_big" : "k_seg_regs");
+  }
+  if (forked) {
+    join_side(fork, 1);
+    if (ntier >= 3) join_side(fork, 2);
   }
   if (max_len > (uint32_t)kBigMax) {  // rare: device-wide radix sort of the longest segments
     uint64_t h[2];
@@ -293,15 +311,16 @@ static void segsort_impl(uint32_t* data, const Seg& sg, uint64_t nseg, uint32_t 
 }
 
 void segmented_sort_u32(uint32_t* data, const uint64_t* off16, const uint32_t* len, uint64_t nseg, uint32_t max_len,
-                        Allocator& al, cudaStream_t s) {
+                        Allocator& al, cudaStream_t s, eh_graph* fork) {
   if (nseg == 0 || max_len <= 1) return;
-  segsort_impl(data, Seg{off16, len, nullptr, nullptr}, nseg, max_len, al, s);
+  segsort_impl(data, Seg{off16, len, nullptr, nullptr}, nseg, max_len, al, s, fork);
 }
 
 void segmented_sort_u32_into(const uint32_t* in, const uint64_t* ioff, uint32_t* out, const uint64_t* off16,
-                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s) {
+                             const uint32_t* len, uint64_t nseg, uint32_t max_len, Allocator& al, cudaStream_t s,
+                             eh_graph* fork) {
   if (nseg == 0 || max_len == 0) return;
-  segsort_impl(out, Seg{off16, len, in, ioff}, nseg, max_len, al, s);
+  segsort_impl(out, Seg{off16, len, in, ioff}, nseg, max_len, al, s, fork);
 }
 
 }  // namespace eh
