@@ -1,6 +1,8 @@
-// ingest.cu -- SURVEY.md §8(a) rows a1-a5: upload, canonicalise, radix sort,
-// dedup (= symmetrisation to a simple undirected graph), degree + (degree, id)
-// rank (dictionary encoding), orientation (symmetric pruning) and CSR.
+// ingest.cu -- SURVEY.md §8(a) rows a1-a5: upload, canonicalise + dedup (=
+// symmetrisation to a simple undirected graph) + degree by the bucketed pass of
+// dedup.cu (or, as an ablation and for 32-bit id spaces, the radix sort of the
+// canonical keys), (degree, id) rank (dictionary encoding), orientation
+// (symmetric pruning) and CSR.
 //
 //  PAPER.md:281-282  dictionary encoding of values to 32-bit ids; "the order of
 //                    dictionary ID assignment affects the density of the sets"
@@ -408,7 +410,7 @@ void build_trie(eh_graph* g, const uint32_t* d_src, const uint32_t* d_dst, uint6
   // EH_TEST_DEDUP=sort: LSD radix sort over the 2b significant bits, unique adjacent
   // keys, degrees from the sorted runs (round-1 default, kept as an ablation and as
   // the path for ids of 32 bits); EH_TEST_DEDUP=hash: one global hash set.
-  static const int dd_mode = [] {
+  const int dd_mode = [] {  // read on every load: a test hook set after the first load must take effect
     const char* e = getenv("EH_TEST_DEDUP");
     return !e ? 0 : (strcmp(e, "sort") == 0 ? 1 : (strcmp(e, "hash") == 0 ? 2 : 0));
   }();

@@ -252,9 +252,13 @@ def test_dedup_ablation_paths(seed, mode, monkeypatch):
     radix sort of the canonical keys) instead of the bucketed on-chip dedup of
     dedup.cu -- same trie, same counts."""
     src, dst = synth.rmat(13, 16, 70 + seed)
+    l0 = eh.launch_count()
     base = _gpu_counts(src, dst)
+    l1 = eh.launch_count()
     monkeypatch.setenv("EH_TEST_DEDUP", mode)
     alt = _gpu_counts(src, dst)
+    l2 = eh.launch_count()
+    assert l2 - l1 != l1 - l0  # the hook is read on every load: another kernel sequence ran
     assert base[:2] == alt[:2] == (oracle.count_triangles(src, dst), oracle.count_4cliques(src, dst))
     assert base[2] == alt[2]
 
