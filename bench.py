@@ -313,6 +313,7 @@ def run_reference(args, cfg, src, dst, n_in):
     t0 = time.perf_counter()
     g = oracle.Graph(src, dst)
     t_ing = time.perf_counter() - t0
+    m_und, n_act = int(g.m), int(g.n_vertices)
     t0 = time.perf_counter()
     probe_count = count(g)  # the first warm-up step's count loop; sizes the mode
     t_probe = time.perf_counter() - t0
@@ -376,7 +377,8 @@ def run_reference(args, cfg, src, dst, n_in):
             "unit": "input edges/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": _workload(cfg, args.query), "n_input": n_in, "reference_step": mode},
+            "config": {"workload": _workload(cfg, args.query), "n_input": n_in, "m_undirected": m_und, "n_active": n_act,
+                       "parallelism": f"{threads} host threads", "reference_step": mode},
             "count": counts.pop() if len(counts) == 1 else sorted(counts),
             "cpu_baseline": {"value": value, "unit": "input edges/s", "cores": threads, "kind": "oracle",
                              "sample": sample, "ingest_s": t_ing, "ingest_threads": 1,
