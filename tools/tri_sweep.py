@@ -1,4 +1,5 @@
-"""Dev aid: time eh_count_triangles on one config under several EH_TRI_CFG values."""
+"""Dev aid: time eh_count_triangles (TRI_QUERY=k4: eh_count_4cliques) on one config under several
+values of an environment switch ("-" = unset); TRI_LIB=path times another build of the library."""
 import os
 import statistics
 import sys
@@ -31,7 +32,7 @@ with torch.cuda.stream(st):
         for r in range(6):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            c = g.count_triangles()
+            c = g.count_4cliques() if os.environ.get("TRI_QUERY") == "k4" else g.count_triangles()
             e1.record(st)
             st.synchronize()
             if r:
