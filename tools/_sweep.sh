@@ -1,8 +1,3 @@
-A=paper_1503_02368_b200/lib/libeh_alt.so
-export TRI_QUERY=k4
-for c in C4 C3 C2; do
-python tools/tri_sweep.py $c EH_DUMMY_VEC -
-TRI_LIB=$A python tools/tri_sweep.py $c EH_DUMMY_SCALAR -
-done
-python tools/tri_sweep.py C4 EH_DUMMY_VEC -
-python -m pytest tests -m gpu -x -q -k "k4 or 4clique or K4 or cliques" 2>&1 | tail -2
+for c in C3 C4 C2 C5; do python tools/load_sweep.py $c EH_DUMMY - - ; done
+EH_TIMING=1 python tools/profile_load.py --reps 3 2>&1 | grep timing | tail -1
+python -m pytest tests -m gpu -x -q -k "bucket or dedup or batch" 2>&1 | tail -2
