@@ -946,9 +946,24 @@ uint64_t count_impl(eh_graph* g) {
     if (const char* e = getenv("EH_TEST_TRI_XCAP")) xcap = (uint32_t)std::max(128, atoi(e));  // test hook: unstaged path
     // the unpruned nest takes the wide shapes on every graph; its SEARCH factor still
     // follows the graph size (L2-resident lists: C3 unpruned 415.6 -> 386.9 ms)
-    if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096)
-      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge, 0);
-    else if (wide && xcap <= 4096 && !getenv("EH_TEST_TRI_XCAP")) {
+    if (kUnpruned && g->n_act <= kWideIds && xcap <= 4096) {
+      // the same mid / big split as the pruned wide shape below (the launches run one after
+      // the other: an unpruned launch ends with a stream synchronisation)
+      uint64_t nmid = 0;
+      // (measured: C3 unpruned 6T 438.6 -> 424.3 ms, -R 624.8 -> 579.7; C4 / C2 unchanged)
+      if (!kBlock && mid_max >= tri_warp_max_degree() + 1) {
+        split = DBuf<uint32_t>(g->alloc, nlarge);
+        uint64_t st2[3];
+        partition_k<2>(nlarge, MidClass{g->desc, g->work + nsmall, mid_max}, MidEmit{g->work + nsmall, split.p}, st2,
+                       g->alloc, s);
+        nmid = st2[1] - st2[0];
+      }
+      launch_cta<16, 16384, 4096, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nlarge - nmid, 0,
+                                                                    nmid ? split.p + nmid : nullptr);
+      if (nmid)
+        launch_cta<4, 2048, 0, kUnpruned, kBlock, 0, kG, 16, true>(g, nsmall, nmid, (mid_max + 255) / 256 * 256, split.p,
+                                                                  nullptr, 3u);
+    } else if (wide && xcap <= 4096 && !getenv("EH_TEST_TRI_XCAP")) {
       // Wide shape, pruned set-level nest: the x with |N+(x)| <= kMidMax take the 4-warp
       // CTAs (8 KB table: one-hash filter + hash table, many CTAs per SM, so the per-x
       // barrier tails overlap), the rest the 16-warp CTAs with the 64 KB table.  The class
