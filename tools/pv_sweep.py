@@ -10,6 +10,10 @@ import torch  # noqa: E402
 import paper_1503_02368_b200 as eh  # noqa: E402
 import synth  # noqa: E402
 
+if os.environ.get("TRI_LIB"):  # dev: time another build of the library
+    import paper_1503_02368_b200.eh as _ehm
+    _ehm.LIB_PATH = os.environ["TRI_LIB"]
+
 name = sys.argv[1]
 settings = sys.argv[2:]
 src, dst = synth.CONFIGS[name].generate()
