@@ -14,10 +14,14 @@
 // (min, max) over b-bit ids.  Its bucket is lo's top bb bits (an MSD radix digit),
 // its residual r = (lo's low b - bb bits) << b | hi fits 31 bits, so a bucket holds
 // all pairs of 2^(b - bb) consecutive lo values.
-//   (1) k_bkt_hist: bucket histogram (one read of src / dst);
-//   (2) exclusive scan -> bucket offsets;
-//   (3) k_bkt_part: every non-loop pair's residual scattered into its bucket (one
-//       read of src / dst, one 4-B write; order within a bucket arbitrary);
+//   (1) k_bkt_hist: bucket histogram in shared memory (one read of src / dst), kept
+//       per (chunk of the input, CTA);
+//   (2) k_bkt_colscan + exclusive scan -> bucket offsets and every (chunk, CTA)'s own
+//       range inside each bucket;
+//   (3) k_bkt_part_smem: every non-loop pair's residual scattered into its bucket with
+//       shared-memory cursors -- no global atomics (one read of src / dst, one 4-B
+//       write; order within a bucket arbitrary).  Above 2^15 buckets (id spaces beyond
+//       ~2^23 ids) the histogram and the cursors are global atomics (k_bkt_part_direct);
 //   (4) k_bkt_dedup: one CTA per bucket inserts the residuals into an on-chip
 //       open-addressing hash set (shared memory; buckets too large for it use a
 //       table in global memory), counts each id's distinct neighbours (lo side in
