@@ -95,7 +95,7 @@ typedef struct {
   uint32_t order;
   /* a7 thread class: the x with 2 <= |N+(x)| <= bin_thread_max (within class 0) run
    * one THREAD per x in the triangle count (their <= C(d, 2) probes are too few to
-   * occupy a warp).  0 -> 8 (4 above 2^24 active ids); 1 disables the class; clamped to
+   * occupy a warp).  0 -> 12 (16 above 2^19 active ids, 4 above 2^24); 1 disables the class; clamped to
    * bin_small_max and to 16.  Counts do not depend on it. */
   uint32_t bin_thread_max;
 } eh_config;

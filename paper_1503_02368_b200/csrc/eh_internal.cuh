@@ -340,7 +340,7 @@ inline void join_side(eh_graph* g, int k) {
 uint64_t count_triangles(eh_graph* g);
 uint32_t tri_warp_max_degree();  // largest |N+(x)| the warp-per-x kernels accept
 uint32_t tri_thread_max_degree();  // largest |N+(x)| the thread-per-x kernel accepts
-constexpr uint32_t kThreadMaxDefault = 8;  // default bin_thread_max (a7 thread class)
+constexpr uint32_t kThreadMaxDefault = 12;  // default bin_thread_max (a7 thread class) up to 2^19 active ids; 16 above, 4 above 2^24
 uint64_t count_4cliques(eh_graph* g);
 // count_pv.cu (NEXT-1): t(v) per rank into a device array; Lollipop / Barbell 128-bit counts
 void triangles_per_vertex(eh_graph* g, unsigned long long* d_t);

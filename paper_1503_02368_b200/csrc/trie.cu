@@ -396,7 +396,9 @@ void build_worklists(eh_graph* g) {
   // default 8, 4 above 2^24 active ids (measured, bin_thread_max 1 / 4 / 8 / 12 / 16: C3 8.39 / 8.01 /
   // 7.88 / 7.84 / 7.90 ms, C4 1.42 / 1.33 / 1.31 / 1.30 / 1.30, C2 0.312 / 0.294 / 0.302 / 0.314 / 0.339,
   // C5 864 / 856 / 864 / 872 / 885)
-  const uint32_t tdef = g->n_act > (1ull << 24) ? 4u : kThreadMaxDefault;
+  // re-measured with the round-2 kernels (8 / 12 / 16): C3 7.90 / 7.79 / 7.72 ms, C4 1.19 / 1.14 / 1.11,
+  // C2 0.248 / 0.235 / 0.260; C5 (2 / 4 / 8) 623 / 619 / 623 -- 16 above 2^19 active ids, 12 below, 4 above 2^24
+  const uint32_t tdef = g->n_act > (1ull << 24) ? 4u : g->n_act > (1ull << 19) ? 16u : kThreadMaxDefault;
   const uint64_t tmax = std::min<uint64_t>(g->bin_thread_max ? g->bin_thread_max : tdef,
                                            std::min<uint64_t>(hi[0] - 1, tri_thread_max_degree()));
   const uint64_t ht = std::max<uint64_t>(2, tmax + 1);
